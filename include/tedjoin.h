@@ -1,0 +1,142 @@
+/* tedjoin — C ABI of the B200 (sm_100a) FP64 epsilon self-join engine.
+ *
+ * This is the boundary below the Python drop-in for the reference package's
+ * `tilejoin.join.self_join(dataset, JoinConfig(epsilon=...)) -> JoinResult`
+ * (/root/reference/pkg/src/tilejoin/join.py:150).  The reference is pure
+ * Python/NumPy and has no FFI of its own; each entry point below names the
+ * reference function whose work it replaces.  A maintainer binds it with
+ * ctypes.
+ *
+ * Conventions
+ *  - every call returns an int status: TJ_OK, or TJ_EINVAL (maps to
+ *    tilejoin.errors.ValidationError), TJ_ECAPACITY (ResourceError),
+ *    TJ_ECUDA / TJ_ENOMEM (RuntimeError).  Message text: tj_last_error().
+ *  - pointers documented "device" are caller-owned CUDA device memory
+ *    (torch tensors' data_ptr()); "host" pointers are plain host memory.
+ *  - `stream` is a cudaStream_t passed as void*; calls that only enqueue work
+ *    are asynchronous, calls documented "synchronous" block on the stream.
+ *  - one tj_ctx per device.  A ctx is not thread-safe; distinct ctxs may be
+ *    driven from distinct host threads.  The ctx owns the grid index, the
+ *    pair-append buffer and all scratch.
+ */
+#ifndef TEDJOIN_H
+#define TEDJOIN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TJ_OK 0
+#define TJ_EINVAL 1
+#define TJ_ECAPACITY 2
+#define TJ_ECUDA 3
+#define TJ_ENOMEM 4
+
+#define TJ_KERNEL_CORE 0 /* CUDA-core FP64 direct form, GDS-Join style ("scalar") */
+#define TJ_KERNEL_DMMA 1 /* mma.sync m8n8k4 f64 expanded form, paper Alg. 2 ("tile") */
+
+/* Largest k_idx the device grid enumerates (3^(k-1) neighbour rows per cell). */
+#define TJ_MAX_K_IDX 8
+/* Largest logical dimensionality the refine kernels are instantiated for. */
+#define TJ_MAX_DIM 128
+
+typedef struct tj_ctx tj_ctx;
+
+typedef struct {
+  int64_t n;                /* points */
+  int32_t d;                /* logical dimensionality */
+  int32_t d_pad;            /* 4*ceil(d/4): row stride of the cell-ordered coordinates */
+  int32_t k_idx;            /* indexed dimensions requested */
+  int32_t key_bits;         /* bits of the packed cell key */
+  double eps;               /* epsilon */
+  double eps_sq;            /* fl(eps*eps), the join threshold (join.py:176) */
+  int64_t n_cells;          /* non-empty cells (GridIndex.n_cells, grid.py:48-50) */
+  int64_t n_runs;           /* contiguous candidate runs over all cells */
+  int64_t candidates;       /* C = sum_cells |cell|*|cand(cell)| (JoinStats.candidates_refined) */
+  int64_t tiles;            /* sum_cells ceil(|cell|/8)*ceil(|cand|/8) (join.py:257-261) */
+  int64_t max_cell;         /* largest cell population */
+} tj_grid_info;
+
+typedef struct {
+  int64_t tiles_processed;    /* DMMA kernel: 8x8 tiles evaluated            (join.py:270) */
+  int64_t chunks_executed;    /* DMMA kernel: 4-dim chunks executed          (join.py:271) */
+  int64_t chunks_skipped;     /* DMMA kernel: chunks skipped by short-circuit (join.py:272) */
+  int64_t candidates_refined; /* candidate pairs refined                     (join.py:273) */
+  int64_t pairs_emitted;      /* result pairs, self-pairs included           (join.py:207) */
+  int64_t guard_rechecks;     /* DMMA pairs re-decided by the exact direct form */
+} tj_stats;
+
+/* ---- context ----------------------------------------------------------- */
+int tj_version(void);
+int tj_ctx_create(int device, tj_ctx** out);
+void tj_ctx_destroy(tj_ctx* ctx);
+/* Message of the last failed call on ctx (or of the last failed tj_ctx_create when ctx is NULL). */
+const char* tj_last_error(const tj_ctx* ctx);
+
+/* ---- grid index: replaces grid.build_index (grid.py:66-101) + kernels.precompute_chunk_norms
+ *      (kernels.py:115-131) + candidates_for_cell for every cell (grid.py:121-133, join.py:169)
+ *      + the per-cell estimate |cell|*|cand| (join.py:170-173).
+ * coords: device, n rows of FP64 coordinates, row stride ld >= d doubles (the
+ * reference Dataset.coords layout is ld = 4*ceil(d/4), datasets.py:46-48).  Only
+ * the first d columns are read.  The grid keeps a cell-ordered zero-padded
+ * copy, chunk norms, the non-empty cell table and the compacted candidate runs.
+ * k_idx in [1, min(d, TJ_MAX_K_IDX)]; eps > 0 finite. */
+int tj_build_grid(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                  int32_t k_idx, double eps, void* stream);
+/* synchronous */
+int tj_get_grid_info(tj_ctx* ctx, tj_grid_info* out);
+
+/* Export the index to host arrays (synchronous).  Any pointer may be NULL.
+ * point_order:  n      original ids in cell order (GridIndex.point_order, grid.py:94)
+ * cell_start:   n_cells+1 offsets into point_order
+ * cell_coords:  n_cells*k_idx int64 cell coordinates, lexicographic (GridIndex.ordered_cells)
+ * cell_cands:   n_cells |cand(cell)|
+ * cell_runs:    n_cells+1 offsets into runs
+ * runs:         n_runs*2 uint32 [begin,end) ranges of cell-ordered positions */
+int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int64_t* cell_coords,
+                   int64_t* cell_cands, int64_t* cell_runs, uint32_t* runs);
+
+/* ---- refine + emit: replaces the per-batch loop of self_join (join.py:184-202) with
+ *      _TileRefiner/distance_tile_v2 (kernel=TJ_KERNEL_DMMA, join.py:238-283, kernels.py:184-263)
+ *      or _ScalarRefiner (kernel=TJ_KERNEL_CORE, join.py:286-349).
+ * Refines the query cells [cell_begin, cell_end) and appends their pairs to the
+ * ctx result buffer.  Asynchronous. */
+int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+              int64_t cell_end, void* stream);
+/* Pairs appended since the last tj_reset_results (synchronous).  If the append
+ * buffer overflowed the ctx grows it and the caller must re-run the batch:
+ * *overflowed is set to 1 and the buffer is left reset. */
+int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed);
+int tj_reset_results(tj_ctx* ctx, void* stream);
+/* Reserve append capacity for `pairs` result pairs (optional; the ctx sizes it itself). */
+int tj_reserve_results(tj_ctx* ctx, int64_t pairs);
+
+/* Canonical output (replaces the concat + lexsort of join.py:203-204): CSR by
+ * original query id with neighbour ids ascending.  offsets: device int64[n+1];
+ * neighbors: device uint32[total].  Only rows of queries refined since the last
+ * reset are non-empty.  Asynchronous. */
+int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream);
+
+/* Counters accumulated since the last tj_reset_results (synchronous). */
+int tj_get_stats(tj_ctx* ctx, tj_stats* out);
+
+/* Per-cell cost |cell|*|cand(cell)| to host (synchronous); feeds plan_batches
+ * (join.py:114-147) and the multi-GPU cost-balanced cell split. */
+int tj_cell_costs(tj_ctx* ctx, int64_t* costs);
+
+/* ---- measurement helpers ------------------------------------------------ */
+/* FP64 throughput microbenchmark on the current device: kind 0 = DFMA,
+ * 1 = DMMA m8n8k4, 2 = both interleaved.  Reports FLOP/s counting 2 per FMA. */
+int tj_fp64_peak(int32_t kind, int32_t iters, double* tflops, double* ms);
+/* One m8n8k4 f64 MMA on device; A 8x4, B 4x8, C/D 8x8 row-major host arrays. */
+int tj_dmma_known_answer(const double* a, const double* b, const double* c, double* d);
+/* Average duration (ms) of the last tj_refine launch's refine kernel, measured
+ * with CUDA events on the launching stream (synchronous). */
+int tj_last_refine_ms(tj_ctx* ctx, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEDJOIN_H */

@@ -1,0 +1,273 @@
+/* ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the reference tilejoin self-join with its scalar
+ * (direct-form) refinement, used as the parity checker for the CUDA path and as
+ * the CPU baseline in bench.py.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it; the product
+ * path (paper_2209_11287_b200) never does.
+ *
+ * Followed reference lines (/root/reference/pkg/src/tilejoin):
+ *   grid.py:81       coords = floor(x[:, :k] / eps)  (IEEE divide, then floor)
+ *   grid.py:83-94    stable lexicographic order of points by cell, dim 0 primary
+ *   grid.py:104-133  candidates = members of the occupied cells at Chebyshev
+ *                    distance <= 1, lexicographic cell order, ids ascending
+ *   join.py:310-318  per query: acc = 0; for dim: diff = q - c; acc += diff*diff;
+ *                    keep acc <= eps*eps  (oracle.py:75-84 is the same sum order)
+ *   join.py:203-204  pairs sorted by (query id, neighbour id)
+ * Compile with -ffp-contract=off so acc + diff*diff is never fused (numpy
+ * evaluates the product and the sum as two correctly rounded operations).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MAXK 16
+
+typedef struct {
+  const int64_t* cc; /* n * k cell coordinates */
+  int k;
+} sort_ctx;
+
+static sort_ctx g_sort; /* qsort has no context argument; sorting is single-threaded */
+
+static int cmp_point(const void* a, const void* b) {
+  const uint32_t i = *(const uint32_t*)a, j = *(const uint32_t*)b;
+  const int64_t* x = g_sort.cc + (int64_t)i * g_sort.k;
+  const int64_t* y = g_sort.cc + (int64_t)j * g_sort.k;
+  for (int t = 0; t < g_sort.k; ++t) {
+    if (x[t] < y[t]) return -1;
+    if (x[t] > y[t]) return 1;
+  }
+  return (i > j) - (i < j); /* stable: ids ascending inside a cell */
+}
+
+static int cmp_coord(const int64_t* x, const int64_t* y, int k) {
+  for (int t = 0; t < k; ++t) {
+    if (x[t] < y[t]) return -1;
+    if (x[t] > y[t]) return 1;
+  }
+  return 0;
+}
+
+static int cmp_u32(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x > y) - (x < y);
+}
+
+typedef struct {
+  int64_t n, n_cells;
+  int k;
+  uint32_t* order;   /* n: point ids in cell order */
+  int64_t* cstart;   /* n_cells + 1 */
+  int64_t* ccoord;   /* n_cells * k */
+} grid_t;
+
+static int build_grid(const double* x, int64_t n, int d, int64_t ld, int k, double eps,
+                      grid_t* g) {
+  (void)d;
+  int64_t* cc = (int64_t*)malloc(sizeof(int64_t) * n * k);
+  g->order = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  if (!cc || !g->order) return -1;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int t = 0; t < k; ++t) cc[i * k + t] = (int64_t)floor(x[i * ld + t] / eps);
+    g->order[i] = (uint32_t)i;
+  }
+  g_sort.cc = cc;
+  g_sort.k = k;
+  qsort(g->order, (size_t)n, sizeof(uint32_t), cmp_point);
+  g->cstart = (int64_t*)malloc(sizeof(int64_t) * (n + 1));
+  g->ccoord = (int64_t*)malloc(sizeof(int64_t) * n * k);
+  int64_t nc = 0;
+  for (int64_t p = 0; p < n; ++p) {
+    const int64_t* c = cc + (int64_t)g->order[p] * k;
+    if (p == 0 || cmp_coord(c, g->ccoord + (nc - 1) * k, k) != 0) {
+      memcpy(g->ccoord + nc * k, c, sizeof(int64_t) * k);
+      g->cstart[nc++] = p;
+    }
+  }
+  g->cstart[nc] = n;
+  g->n = n;
+  g->n_cells = nc;
+  g->k = k;
+  free(cc);
+  return 0;
+}
+
+static void free_grid(grid_t* g) {
+  free(g->order);
+  free(g->cstart);
+  free(g->ccoord);
+}
+
+static int64_t find_cell(const grid_t* g, const int64_t* c) {
+  int64_t lo = 0, hi = g->n_cells;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) / 2;
+    int r = cmp_coord(g->ccoord + mid * g->k, c, g->k);
+    if (r == 0) return mid;
+    if (r < 0) lo = mid + 1;
+    else hi = mid;
+  }
+  return -1;
+}
+
+/* Occupied neighbour cells of cell `ci`, lexicographic (itertools.product order). */
+static int neighbours(const grid_t* g, int64_t ci, int64_t* out) {
+  const int k = g->k;
+  int64_t nb[MAXK];
+  int cnt = 0;
+  int total = 1;
+  for (int t = 0; t < k; ++t) total *= 3;
+  for (int r = 0; r < total; ++r) {
+    int rr = r;
+    for (int t = k - 1; t >= 0; --t) {
+      nb[t] = g->ccoord[ci * k + t] + (rr % 3) - 1;
+      rr /= 3;
+    }
+    int64_t f = find_cell(g, nb);
+    if (f >= 0) out[cnt++] = f;
+  }
+  return cnt;
+}
+
+static inline int direct_le(const double* x, int64_t ld, int d, uint32_t q, uint32_t c,
+                            double eps_sq) {
+  const double* a = x + (int64_t)q * ld;
+  const double* b = x + (int64_t)c * ld;
+  double acc = 0.0;
+  for (int t = 0; t < d; ++t) {
+    double diff = a[t] - b[t];
+    acc = acc + diff * diff;
+  }
+  return acc <= eps_sq;
+}
+
+/* Squared distance in the reference order (exported for boundary classification). */
+double oracle_sqdist(const double* x, int64_t ld, int d, int64_t q, int64_t c) {
+  const double* a = x + q * ld;
+  const double* b = x + c * ld;
+  double acc = 0.0;
+  for (int t = 0; t < d; ++t) {
+    double diff = a[t] - b[t];
+    acc = acc + diff * diff;
+  }
+  return acc;
+}
+
+/* Refine the query cells listed in `cells` (or all cells when cells == NULL).
+ * Pass 1 (nbrs == NULL): counts[q] = |R(q)| for every query in those cells.
+ * Pass 2: writes each row at nbrs[offsets[q]...] ascending. */
+static void refine_cells(const grid_t* g, const double* x, int64_t ld, int d, double eps_sq,
+                         const int64_t* cells, int64_t n_sel, int64_t* counts,
+                         const int64_t* offsets, uint32_t* nbrs, int threads) {
+  int max_nb = 1;
+  for (int t = 0; t < g->k; ++t) max_nb *= 3;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+  {
+    int64_t* nb = (int64_t*)malloc(sizeof(int64_t) * max_nb);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t s = 0; s < n_sel; ++s) {
+      const int64_t ci = cells ? cells[s] : s;
+      const int nn = neighbours(g, ci, nb);
+      for (int64_t qp = g->cstart[ci]; qp < g->cstart[ci + 1]; ++qp) {
+        const uint32_t q = g->order[qp];
+        int64_t cnt = 0;
+        uint32_t* row = nbrs ? nbrs + offsets[q] : NULL;
+        for (int m = 0; m < nn; ++m) {
+          for (int64_t cp = g->cstart[nb[m]]; cp < g->cstart[nb[m] + 1]; ++cp) {
+            const uint32_t c = g->order[cp];
+            if (direct_le(x, ld, d, q, c, eps_sq)) {
+              if (row) row[cnt] = c;
+              ++cnt;
+            }
+          }
+        }
+        if (row) qsort(row, (size_t)cnt, sizeof(uint32_t), cmp_u32);
+        else counts[q] = cnt;
+      }
+    }
+    free(nb);
+  }
+}
+
+/* Grid summary for parity of the device index (grid.py semantics).
+ * Returns n_cells; fills point_order (n), cell_start (n_cells+1, caller sized n+1),
+ * cell_coords (n_cells*k, caller sized n*k) when non-NULL, and per-cell candidate
+ * counts (n_cells) when cand != NULL. */
+int64_t oracle_grid(const double* x, int64_t n, int d, int64_t ld, int k, double eps,
+                    uint32_t* point_order, int64_t* cell_start, int64_t* cell_coords,
+                    int64_t* cand) {
+  grid_t g;
+  if (k < 1 || k > MAXK || build_grid(x, n, d, ld, k, eps, &g) != 0) return -1;
+  if (point_order) memcpy(point_order, g.order, sizeof(uint32_t) * n);
+  if (cell_start) memcpy(cell_start, g.cstart, sizeof(int64_t) * (g.n_cells + 1));
+  if (cell_coords) memcpy(cell_coords, g.ccoord, sizeof(int64_t) * g.n_cells * k);
+  if (cand) {
+    int max_nb = 1;
+    for (int t = 0; t < k; ++t) max_nb *= 3;
+    int64_t* nb = (int64_t*)malloc(sizeof(int64_t) * max_nb);
+    for (int64_t c = 0; c < g.n_cells; ++c) {
+      int nn = neighbours(&g, c, nb);
+      int64_t s = 0;
+      for (int m = 0; m < nn; ++m) s += g.cstart[nb[m] + 1] - g.cstart[nb[m]];
+      cand[c] = s;
+    }
+    free(nb);
+  }
+  int64_t nc = g.n_cells;
+  free_grid(&g);
+  return nc;
+}
+
+/* Full (or cell-sampled) self-join.  Output CSR by original id: offsets[n+1]
+ * (rows of unselected queries are empty), neighbours ascending.  Two calls:
+ * first with nbrs == NULL to get *total, then with a buffer of *total ids.
+ * sel_cells: indices into the lexicographic cell list (NULL = all cells). */
+int oracle_self_join(const double* x, int64_t n, int d, int64_t ld, int k, double eps,
+                     const int64_t* sel_cells, int64_t n_sel, int64_t* offsets,
+                     uint32_t* nbrs, int64_t* total, int threads) {
+  grid_t g;
+  if (k < 1 || k > MAXK || build_grid(x, n, d, ld, k, eps, &g) != 0) return -1;
+  const double eps_sq = eps * eps;
+  const int64_t m = sel_cells ? n_sel : g.n_cells;
+  if (sel_cells) {
+    for (int64_t s = 0; s < n_sel; ++s)
+      if (sel_cells[s] < 0 || sel_cells[s] >= g.n_cells) {
+        free_grid(&g);
+        return -2;
+      }
+  }
+  if (!nbrs) {
+    int64_t* counts = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+    refine_cells(&g, x, ld, d, eps_sq, sel_cells, m, counts, NULL, NULL, threads);
+    int64_t acc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      offsets[i] = acc;
+      acc += counts[i];
+    }
+    offsets[n] = acc;
+    *total = acc;
+    free(counts);
+  } else {
+    refine_cells(&g, x, ld, d, eps_sq, sel_cells, m, NULL, offsets, nbrs, threads);
+  }
+  free_grid(&g);
+  return 0;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

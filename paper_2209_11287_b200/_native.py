@@ -1,0 +1,222 @@
+"""ctypes binding of libtedjoin.so (include/tedjoin.h) and the per-device context.
+
+The CUDA library is the only compute path: if it cannot be loaded, or no CUDA
+device is visible, every entry point raises RuntimeError — there is no CPU
+fallback.  Device buffers are torch tensors (data_ptr()), streams are torch's
+current CUDA stream on the context's device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .errors import ResourceError, ValidationError
+
+LIB_PATH = Path(__file__).resolve().parent / "libtedjoin.so"
+
+TJ_OK, TJ_EINVAL, TJ_ECAPACITY, TJ_ECUDA, TJ_ENOMEM = 0, 1, 2, 3, 4
+TJ_KERNEL_CORE, TJ_KERNEL_DMMA = 0, 1
+TJ_MAX_K_IDX = 8
+TJ_MAX_DIM = 128
+
+_i32, _i64, _f64, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+
+
+class GridInfo(ctypes.Structure):
+    _fields_ = [
+        ("n", _i64), ("d", _i32), ("d_pad", _i32), ("k_idx", _i32), ("key_bits", _i32),
+        ("eps", _f64), ("eps_sq", _f64), ("n_cells", _i64), ("n_runs", _i64),
+        ("candidates", _i64), ("tiles", _i64), ("max_cell", _i64),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("tiles_processed", _i64), ("chunks_executed", _i64), ("chunks_skipped", _i64),
+        ("candidates_refined", _i64), ("pairs_emitted", _i64), ("guard_rechecks", _i64),
+    ]
+
+
+# name -> (restype, argtypes); every symbol include/tedjoin.h declares
+SIGNATURES = {
+    "tj_version": (_i32, []),
+    "tj_ctx_create": (_i32, [_i32, ctypes.POINTER(_vp)]),
+    "tj_ctx_destroy": (None, [_vp]),
+    "tj_last_error": (ctypes.c_char_p, [_vp]),
+    "tj_build_grid": (_i32, [_vp, _vp, _i64, _i32, _i64, _i32, _f64, _vp]),
+    "tj_get_grid_info": (_i32, [_vp, ctypes.POINTER(GridInfo)]),
+    "tj_grid_export": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "tj_refine": (_i32, [_vp, _i32, _i32, _i64, _i64, _vp]),
+    "tj_result_count": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+    "tj_reset_results": (_i32, [_vp, _vp]),
+    "tj_reserve_results": (_i32, [_vp, _i64]),
+    "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
+    "tj_get_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
+    "tj_cell_costs": (_i32, [_vp, _vp]),
+    "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
+    "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
+    "tj_last_refine_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libtedjoin.so and bind every declared symbol (no GPU needed)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is missing: build the CUDA extension first "
+                "(python -m paper_2209_11287_b200.build); there is no CPU fallback"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _raise(status: int, msg: str):
+    if status == TJ_EINVAL:
+        raise ValidationError(msg)
+    if status == TJ_ECAPACITY:
+        raise ResourceError(msg)
+    raise RuntimeError(f"tedjoin CUDA error ({status}): {msg}")
+
+
+class Context:
+    """One tj_ctx on one CUDA device (owns the device grid and result buffers)."""
+
+    def __init__(self, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("tedjoin requires a CUDA device (sm_100a); none is visible")
+        self.lib = load_library()
+        self.device = int(device)
+        handle = _vp()
+        st = self.lib.tj_ctx_create(self.device, ctypes.byref(handle))
+        if st != TJ_OK:
+            _raise(st, self.lib.tj_last_error(None).decode())
+        self.handle = handle
+        self.lock = threading.RLock()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and getattr(self, "lib", None) is not None:
+            try:
+                self.lib.tj_ctx_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def _check(self, st: int):
+        if st != TJ_OK:
+            _raise(st, self.lib.tj_last_error(self.handle).decode())
+
+    def stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device)
+
+    def build_grid(self, coords, n: int, d: int, ld: int, k_idx: int, eps: float, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_build_grid(self.handle, coords.data_ptr(), n, d, ld, k_idx,
+                                           float(eps), s.cuda_stream))
+
+    def grid_info(self) -> GridInfo:
+        info = GridInfo()
+        self._check(self.lib.tj_get_grid_info(self.handle, ctypes.byref(info)))
+        return info
+
+    def export(self, info: GridInfo, k: int):
+        import numpy as np
+
+        order = np.empty(info.n, dtype=np.uint32)
+        cstart = np.empty(info.n_cells + 1, dtype=np.int64)
+        coords = np.empty((info.n_cells, k), dtype=np.int64)
+        cands = np.empty(info.n_cells, dtype=np.int64)
+        cruns = np.empty(info.n_cells + 1, dtype=np.int64)
+        runs = np.empty((max(info.n_runs, 1), 2), dtype=np.uint32)
+        self._check(self.lib.tj_grid_export(
+            self.handle, order.ctypes.data, cstart.ctypes.data, coords.ctypes.data,
+            cands.ctypes.data, cruns.ctypes.data, runs.ctypes.data))
+        return order, cstart, coords, cands, cruns, runs[: info.n_runs]
+
+    def cell_costs(self, n_cells: int):
+        import numpy as np
+
+        out = np.empty(n_cells, dtype=np.int64)
+        self._check(self.lib.tj_cell_costs(self.handle, out.ctypes.data))
+        return out
+
+    def refine(self, kernel: int, short_circuit: bool, cell_begin: int, cell_end: int, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_refine(self.handle, kernel, int(bool(short_circuit)),
+                                       cell_begin, cell_end, s.cuda_stream))
+
+    def reset_results(self, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_reset_results(self.handle, s.cuda_stream))
+
+    def reserve_results(self, pairs: int):
+        self._check(self.lib.tj_reserve_results(self.handle, int(pairs)))
+
+    def result_count(self):
+        total, over = _i64(), _i32()
+        self._check(self.lib.tj_result_count(self.handle, ctypes.byref(total), ctypes.byref(over)))
+        return int(total.value), bool(over.value)
+
+    def finalize(self, offsets, neighbors, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_finalize(self.handle, offsets.data_ptr(),
+                                         neighbors.data_ptr() if neighbors is not None else None,
+                                         s.cuda_stream))
+
+    def stats(self) -> Stats:
+        st = Stats()
+        self._check(self.lib.tj_get_stats(self.handle, ctypes.byref(st)))
+        return st
+
+    def last_refine_ms(self) -> float:
+        ms = _f64()
+        self._check(self.lib.tj_last_refine_ms(self.handle, ctypes.byref(ms)))
+        return float(ms.value)
+
+
+_contexts: dict[int, Context] = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device: int | None = None) -> Context:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("tedjoin requires a CUDA device (sm_100a); none is visible")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    with _ctx_lock:
+        ctx = _contexts.get(dev)
+        if ctx is None:
+            ctx = _contexts[dev] = Context(dev)
+        return ctx
+
+
+def fp64_peak(kind: int, iters: int = 8192) -> tuple[float, float]:
+    """(TFLOP/s, ms) of the FP64 microbenchmark on the current device."""
+    lib = load_library()
+    tf, ms = _f64(), _f64()
+    st = lib.tj_fp64_peak(kind, iters, ctypes.byref(tf), ctypes.byref(ms))
+    if st != TJ_OK:
+        raise RuntimeError(f"tj_fp64_peak failed with status {st}")
+    return float(tf.value), float(ms.value)

@@ -1,0 +1,365 @@
+// extern "C" entry points of libtedjoin.so (declared in include/tedjoin.h).
+// Every entry point converts internal failures into a status code and keeps
+// the message for tj_last_error(); no C++ exception crosses the ABI.
+#include <cmath>
+#include <mutex>
+
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace tj {
+
+[[noreturn]] void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+static std::mutex g_err_mu;
+static std::string g_err;  // failures without a ctx (tj_ctx_create)
+
+template <class F>
+static int guarded(tj_ctx* ctx, F&& f) {
+  try {
+    if (ctx) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (cur != ctx->device) TJ_CUDA(cudaSetDevice(ctx->device));
+    }
+    f();
+    return TJ_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->err = e.msg;
+    else {
+      std::lock_guard<std::mutex> lk(g_err_mu);
+      g_err = e.msg;
+    }
+    return e.status;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return TJ_ECUDA;
+  }
+}
+
+static DevCounters* counters(tj_ctx* ctx) { return ctx->counters.as<DevCounters>(); }
+
+static void require_grid(tj_ctx* ctx) {
+  if (!ctx->g.built) fail(TJ_EINVAL, "no grid has been built on this context");
+}
+
+static void zero_results(tj_ctx* ctx, cudaStream_t s) {
+  ctx->counters.ensure(sizeof(DevCounters), s);
+  TJ_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(DevCounters), s));
+  if (ctx->g.n > 0) {
+    ctx->qcount.ensure(sizeof(uint32_t) * ctx->g.n, s);
+    TJ_CUDA(cudaMemsetAsync(ctx->qcount.ptr, 0, sizeof(uint32_t) * ctx->g.n, s));
+  }
+}
+
+static void reserve_pairs(tj_ctx* ctx, unsigned long long pairs, cudaStream_t s) {
+  pairs = std::max<unsigned long long>(pairs, 1024);
+  if (pairs <= ctx->pair_cap) return;
+  ctx->pairs.release(s);
+  ctx->pair_cap = 0;
+  ctx->pairs.ensure(sizeof(uint2) * pairs, s);
+  ctx->pair_cap = pairs;
+}
+
+// Guard-band half-width relative to |q|^2 + max|c|^2 (+eps^2); see refine_dmma.cu.
+static double guard_rel(int d, int d_pad) { return (4.0 * d_pad + 4.0 * d + 64.0) * std::ldexp(1.0, -53); }
+
+}  // namespace tj
+
+using namespace tj;
+
+extern "C" {
+
+int tj_version(void) { return 100; }
+
+int tj_ctx_create(int device, tj_ctx** out) {
+  if (!out) return TJ_EINVAL;
+  *out = nullptr;
+  return guarded(nullptr, [&] {
+    int count = 0;
+    TJ_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      fail(TJ_EINVAL, "device " + std::to_string(device) + " out of range (" +
+                          std::to_string(count) + " visible)");
+    TJ_CUDA(cudaSetDevice(device));
+    cudaMemPool_t pool;
+    TJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;  // keep freed blocks cached: repeated joins allocate nothing
+    TJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    tj_ctx* c = new tj_ctx();
+    c->device = device;
+    cudaEventCreate(&c->ev0);
+    cudaEventCreate(&c->ev1);
+    *out = c;
+  });
+}
+
+void tj_ctx_destroy(tj_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&ctx->P,        &ctx->NRM,       &ctx->CN,       &ctx->perm,      &ctx->keys,
+                    &ctx->cell_key, &ctx->cell_start, &ctx->cell_runs, &ctx->runs,      &ctx->run_off,
+                    &ctx->cell_cand, &ctx->cell_cost, &ctx->keys_alt,  &ctx->vals_alt,  &ctx->sort_hist,
+                    &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
+                    &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill};
+  for (DevBuf* b : bufs) b->release(0);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaDeviceSynchronize();
+  delete ctx;
+}
+
+const char* tj_last_error(const tj_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_err.c_str();
+}
+
+int tj_build_grid(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                  int32_t k_idx, double eps, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n < 1 || d < 1) fail(TJ_EINVAL, "need n >= 1 and d >= 1");
+    if (n >= (int64_t(1) << 32) - 1) fail(TJ_EINVAL, "n must be < 2^32 - 1 (32-bit point ids)");
+    if (d > TJ_MAX_DIM) fail(TJ_EINVAL, "d must be <= " + std::to_string(TJ_MAX_DIM));
+    if (!(std::isfinite(eps) && eps > 0))
+      fail(TJ_EINVAL, "epsilon must be positive and finite");
+    if (k_idx < 1 || k_idx > d)
+      fail(TJ_EINVAL, "k_idx must be in [1, " + std::to_string(d) + "], got " +
+                          std::to_string(k_idx));
+    if (k_idx > TJ_MAX_K_IDX)
+      fail(TJ_EINVAL, "k_idx must be <= " + std::to_string(TJ_MAX_K_IDX) +
+                          " on the device grid, got " + std::to_string(k_idx));
+    if (!coords) fail(TJ_EINVAL, "coords is null");
+    if (ld < d) fail(TJ_EINVAL, "ld must be >= d");
+    build_grid(ctx, coords, n, d, ld, k_idx, eps, s);
+    zero_results(ctx, s);
+    ctx->last_stream = s;
+  });
+}
+
+int tj_get_grid_info(tj_ctx* ctx, tj_grid_info* out) {
+  if (!ctx || !out) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    const GridState& g = ctx->g;
+    out->n = g.n;
+    out->d = g.d;
+    out->d_pad = g.d_pad;
+    out->k_idx = g.k;
+    out->key_bits = g.key_bits;
+    out->eps = g.eps;
+    out->eps_sq = g.eps_sq;
+    out->n_cells = g.n_cells;
+    out->n_runs = g.n_runs;
+    out->candidates = g.candidates;
+    out->tiles = g.tiles;
+    out->max_cell = g.max_cell;
+  });
+}
+
+// Decode packed cell keys back into cell coordinates.
+__global__ void decode_keys_kernel(const uint64_t* keys, int64_t n_cells, int k,
+                                   const int* shift, const long long* cmin, int64_t* out) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    for (int j = 0; j < k; ++j) {
+      const int hi = j == 0 ? 64 : shift[j - 1];
+      const int bits = hi - shift[j];
+      const uint64_t f = (keys[c] >> shift[j]) & (bits >= 64 ? ~0ull : ((1ull << bits) - 1));
+      out[c * k + j] = int64_t(f) - 1 + cmin[j];
+    }
+  }
+}
+
+int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int64_t* cell_coords,
+                   int64_t* cell_cands, int64_t* cell_runs, uint32_t* runs) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    const GridState& g = ctx->g;
+    cudaStream_t s = ctx->last_stream;
+    TJ_CUDA(cudaStreamSynchronize(s));
+    if (point_order)
+      TJ_CUDA(cudaMemcpy(point_order, ctx->perm.ptr, sizeof(uint32_t) * g.n, cudaMemcpyDeviceToHost));
+    if (cell_start)
+      TJ_CUDA(cudaMemcpy(cell_start, ctx->cell_start.ptr, sizeof(int64_t) * (g.n_cells + 1),
+                         cudaMemcpyDeviceToHost));
+    if (cell_cands)
+      TJ_CUDA(cudaMemcpy(cell_cands, ctx->cell_cand.ptr, sizeof(int64_t) * g.n_cells,
+                         cudaMemcpyDeviceToHost));
+    if (cell_runs)
+      TJ_CUDA(cudaMemcpy(cell_runs, ctx->cell_runs.ptr, sizeof(int64_t) * (g.n_cells + 1),
+                         cudaMemcpyDeviceToHost));
+    if (runs)
+      TJ_CUDA(cudaMemcpy(runs, ctx->runs.ptr, sizeof(uint2) * g.n_runs, cudaMemcpyDeviceToHost));
+    if (cell_coords) {
+      DevBuf tmp;
+      tmp.ensure(sizeof(int64_t) * g.n_cells * g.k + 128 * 2, s);
+      int* dshift = reinterpret_cast<int*>(tmp.as<char>() + sizeof(int64_t) * g.n_cells * g.k);
+      long long* dcmin = reinterpret_cast<long long*>(dshift + 16);
+      int hshift[TJ_MAX_K_IDX];
+      long long hcmin[TJ_MAX_K_IDX];
+      for (int j = 0; j < g.k; ++j) {
+        hshift[j] = g.shift[j];
+        hcmin[j] = g.cmin[j];
+      }
+      TJ_CUDA(cudaMemcpyAsync(dshift, hshift, sizeof(int) * g.k, cudaMemcpyHostToDevice, s));
+      TJ_CUDA(cudaMemcpyAsync(dcmin, hcmin, sizeof(long long) * g.k, cudaMemcpyHostToDevice, s));
+      decode_keys_kernel<<<256, 256, 0, s>>>(ctx->cell_key.as<uint64_t>(), g.n_cells, g.k, dshift,
+                                             dcmin, tmp.as<int64_t>());
+      TJ_CHECK_LAUNCH();
+      TJ_CUDA(cudaMemcpyAsync(cell_coords, tmp.ptr, sizeof(int64_t) * g.n_cells * g.k,
+                              cudaMemcpyDeviceToHost, s));
+      TJ_CUDA(cudaStreamSynchronize(s));
+      tmp.release(s);
+    }
+  });
+}
+
+int tj_reserve_results(tj_ctx* ctx, int64_t pairs) {
+  if (!ctx || pairs < 0) return TJ_EINVAL;
+  return guarded(ctx, [&] { reserve_pairs(ctx, (unsigned long long)pairs, ctx->last_stream); });
+}
+
+int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+              int64_t cell_end, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    const GridState& g = ctx->g;
+    if (kernel != TJ_KERNEL_CORE && kernel != TJ_KERNEL_DMMA)
+      fail(TJ_EINVAL, "kernel must be TJ_KERNEL_CORE or TJ_KERNEL_DMMA");
+    if (cell_begin < 0 || cell_end > g.n_cells || cell_begin > cell_end)
+      fail(TJ_EINVAL, "cell range out of bounds");
+    ctx->have_refine_timing = false;
+    if (cell_begin == cell_end) return;
+    // The expanded form needs finite norms; beyond that the exact kernel decides.
+    const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
+    const bool dmma = kernel == TJ_KERNEL_DMMA && norms_ok && g.d <= 64;
+    if (ctx->pair_cap == 0) {
+      size_t free_b = 0, total_b = 0;
+      TJ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const unsigned long long budget = (unsigned long long)(0.35 * double(free_b)) / sizeof(uint2);
+      reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
+    }
+    const int qpi = dmma ? dmma_queries_per_item(g.d, g.d_pad) : core_queries_per_item(g.d, g.d_pad);
+    const int64_t target = std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
+    ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s);
+    TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
+    RefineArgs a{};
+    a.P = ctx->P.as<double>();
+    a.NRM = ctx->NRM.as<double>();
+    a.CN = ctx->CN.as<double>();
+    a.runs = ctx->runs.as<uint2>();
+    a.run_off = ctx->run_off.as<uint32_t>();
+    a.cell_runs = ctx->cell_runs.as<int64_t>();
+    a.cell_start = ctx->cell_start.as<int64_t>();
+    a.items = ctx->items.as<WorkItem>();
+    a.n_items = ctx->n_items;
+    a.ctr = counters(ctx);
+    a.pairs = ctx->pairs.as<uint2>();
+    a.pair_cap = ctx->pair_cap;
+    a.qcount = ctx->qcount.as<uint32_t>();
+    a.d = g.d;
+    a.d_pad = g.d_pad;
+    a.nchunks = g.nchunks;
+    a.eps_sq = g.eps_sq;
+    a.guard_rel = guard_rel(g.d, g.d_pad);
+    a.max_norm = g.max_norm + g.eps_sq;
+    a.short_circuit = short_circuit ? 1 : 0;
+    TJ_CUDA(cudaEventRecord(ctx->ev0, s));
+    if (dmma) launch_refine_dmma(a, s);
+    else launch_refine_core(a, s);
+    TJ_CUDA(cudaEventRecord(ctx->ev1, s));
+    ctx->have_refine_timing = true;
+  });
+}
+
+int tj_last_refine_ms(tj_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (!ctx->have_refine_timing) fail(TJ_EINVAL, "no refine launch recorded");
+    TJ_CUDA(cudaEventSynchronize(ctx->ev1));
+    float t = 0;
+    TJ_CUDA(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+    *ms = t;
+  });
+}
+
+int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed) {
+  if (!ctx || !total) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = ctx->last_stream;
+    unsigned long long p = 0;
+    TJ_CUDA(cudaMemcpyAsync(&p, &counters(ctx)->pairs, sizeof(p), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaStreamSynchronize(s));
+    *total = int64_t(p);
+    const bool over = p > ctx->pair_cap;
+    if (overflowed) *overflowed = over ? 1 : 0;
+    if (over) {
+      reserve_pairs(ctx, p + p / 8, s);
+      zero_results(ctx, s);
+    }
+  });
+}
+
+int tj_reset_results(tj_ctx* ctx, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    zero_results(ctx, s);
+  });
+}
+
+int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream) {
+  if (!ctx || !offsets) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    unsigned long long p = 0;
+    TJ_CUDA(cudaMemcpyAsync(&p, &counters(ctx)->pairs, sizeof(p), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaStreamSynchronize(s));
+    if (p > ctx->pair_cap)
+      fail(TJ_ECAPACITY, "pair buffer overflowed; call tj_result_count and re-run the batch");
+    if (p > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
+    finalize_csr(ctx, offsets, neighbors, int64_t(p), s);
+  });
+}
+
+int tj_get_stats(tj_ctx* ctx, tj_stats* out) {
+  if (!ctx || !out) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    DevCounters c{};
+    cudaStream_t s = ctx->last_stream;
+    TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaStreamSynchronize(s));
+    out->tiles_processed = int64_t(c.tiles);
+    out->chunks_executed = int64_t(c.chunks_exec);
+    out->chunks_skipped = int64_t(c.chunks_skip);
+    out->candidates_refined = int64_t(c.refined);
+    out->pairs_emitted = int64_t(c.pairs);
+    out->guard_rechecks = int64_t(c.rechecks);
+  });
+}
+
+int tj_cell_costs(tj_ctx* ctx, int64_t* costs) {
+  if (!ctx || !costs) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    TJ_CUDA(cudaStreamSynchronize(ctx->last_stream));
+    TJ_CUDA(cudaMemcpy(costs, ctx->cell_cost.ptr, sizeof(int64_t) * ctx->g.n_cells,
+                       cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

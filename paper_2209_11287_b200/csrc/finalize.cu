@@ -1,0 +1,264 @@
+// Canonical output: CSR by original query id with neighbour ids ascending.
+//
+// Replaces the concatenate + np.lexsort((j, i)) of join.py:203-204.  The refine
+// kernels append (query position, candidate position) pairs in arbitrary order
+// and count pairs per query position.  Here:
+//   1. row counts move from cell order to original-id order and are scanned
+//      into int64 row offsets;
+//   2. every pair is scattered to its row (per-row atomic cursor) as the
+//      original neighbour id;
+//   3. each row is sorted: one warp per row of <= 256 ids (register bitonic
+//      network), one CTA per row of <= 8192 ids (shared-memory bitonic), and a
+//      composite-key radix sort for anything larger.
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace tj {
+
+__global__ void counts_to_orig_kernel(const uint32_t* __restrict__ qcount,
+                                      const uint32_t* __restrict__ perm, int64_t n,
+                                      int64_t* __restrict__ cnt_orig) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
+       p += int64_t(gridDim.x) * blockDim.x)
+    cnt_orig[perm[p]] = qcount[p];
+}
+
+__global__ void scatter_pairs_kernel(const uint2* __restrict__ pairs, int64_t total,
+                                     const uint32_t* __restrict__ perm,
+                                     const int64_t* __restrict__ offsets,
+                                     uint32_t* __restrict__ fill, uint32_t* __restrict__ nbr) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const uint2 pr = pairs[e];
+    const uint32_t row = perm[pr.x];
+    const uint32_t slot = atomicAdd(&fill[row], 1u);
+    nbr[offsets[row] + slot] = perm[pr.y];
+  }
+}
+
+// Bitonic sort of 32*R keys held as v[r] (element index r*32 + lane), ascending.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[R]) {
+  const int lane = lane_id();
+  constexpr int N = 32 * R;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int p = r ^ rj;
+          if (p > r) {
+            const int i = r * 32 + lane;
+            const bool asc = (i & k) == 0;
+            const uint32_t a = v[r], b = v[p];
+            const bool swap = asc ? (a > b) : (a < b);
+            v[r] = swap ? b : a;
+            v[p] = swap ? a : b;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = r * 32 + lane;
+          const bool asc = (i & k) == 0;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool lower = (lane & j) == 0;
+          // lower element keeps min when ascending, max when descending
+          const uint32_t mn = min(v[r], o), mx = max(v[r], o);
+          v[r] = (lower == asc) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_row(uint32_t* row, int len) {
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane_id();
+    v[r] = i < len ? row[i] : 0xffffffffu;
+  }
+  warp_bitonic<R>(v);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane_id();
+    if (i < len) row[i] = v[r];
+  }
+}
+
+constexpr int kWarpSortMax = 256;
+constexpr int kBlockSortMax = 8192;
+
+__global__ void sort_rows_warp_kernel(const int64_t* __restrict__ offsets, int64_t n,
+                                      uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
+                                      unsigned long long* n_big) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n; i += warps) {
+    const int64_t b = offsets[i];
+    const int64_t len = offsets[i + 1] - b;
+    if (len <= 1) continue;
+    uint32_t* row = nbr + b;
+    if (len <= 32) warp_sort_row<1>(row, int(len));
+    else if (len <= 64) warp_sort_row<2>(row, int(len));
+    else if (len <= 128) warp_sort_row<4>(row, int(len));
+    else if (len <= kWarpSortMax) warp_sort_row<8>(row, int(len));
+    else if (lane_id() == 0) big_rows[atomicAdd(n_big, 1ull)] = uint32_t(i);
+  }
+}
+
+// One CTA per listed row of 257..8192 ids: shared-memory bitonic sort.
+__global__ void __launch_bounds__(1024)
+    sort_rows_block_kernel(const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
+                           const uint32_t* __restrict__ rows, const unsigned long long* n_rows,
+                           uint32_t* __restrict__ huge_rows, unsigned long long* n_huge) {
+  __shared__ uint32_t s[kBlockSortMax];
+  for (unsigned long long ri = blockIdx.x; ri < *n_rows; ri += gridDim.x) {
+    const uint32_t i = rows[ri];
+    const int64_t b = offsets[i];
+    const int64_t len = offsets[i + 1] - b;
+    if (len > kBlockSortMax) {
+      if (threadIdx.x == 0) huge_rows[atomicAdd(n_huge, 1ull)] = i;
+      continue;
+    }
+    int N = 512;
+    while (N < len) N <<= 1;
+    __syncthreads();
+    for (int t = threadIdx.x; t < N; t += blockDim.x) s[t] = t < len ? nbr[b + t] : 0xffffffffu;
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = threadIdx.x; t < N; t += blockDim.x) {
+          const int p = t ^ j;
+          if (p > t) {
+            const bool asc = (t & k) == 0;
+            const uint32_t x = s[t], y = s[p];
+            if (asc ? (x > y) : (x < y)) {
+              s[t] = y;
+              s[p] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int t = threadIdx.x; t < len; t += blockDim.x) nbr[b + t] = s[t];
+  }
+}
+
+// Rows longer than kBlockSortMax: gather (row rank << 32 | id) keys, radix sort, scatter back.
+__global__ void huge_gather_kernel(const int64_t* __restrict__ offsets, const uint32_t* nbr,
+                                   const uint32_t* __restrict__ huge, int n_huge,
+                                   const int64_t* __restrict__ base, uint64_t* __restrict__ keys) {
+  for (int h = blockIdx.y; h < n_huge; h += gridDim.y) {
+    const int64_t b = offsets[huge[h]];
+    const int64_t len = offsets[huge[h] + 1] - b;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < len;
+         t += int64_t(gridDim.x) * blockDim.x)
+      keys[base[h] + t] = (uint64_t(h) << 32) | nbr[b + t];
+  }
+}
+__global__ void huge_scatter_kernel(const int64_t* __restrict__ offsets, uint32_t* nbr,
+                                    const uint32_t* __restrict__ huge, int n_huge,
+                                    const int64_t* __restrict__ base,
+                                    const uint64_t* __restrict__ keys) {
+  for (int h = blockIdx.y; h < n_huge; h += gridDim.y) {
+    const int64_t b = offsets[huge[h]];
+    const int64_t len = offsets[huge[h] + 1] - b;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < len;
+         t += int64_t(gridDim.x) * blockDim.x)
+      nbr[b + t] = uint32_t(keys[base[h] + t]);
+  }
+}
+
+static unsigned blocks_for(int64_t n, int threads) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), kNumSMs * 16)));
+}
+
+void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t total, cudaStream_t s) {
+  const int64_t n = ctx->g.n;
+  ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
+  int64_t* cnt = ctx->tmp64.as<int64_t>();
+  counts_to_orig_kernel<<<blocks_for(n, 256), 256, 0, s>>>(ctx->qcount.as<uint32_t>(),
+                                                          ctx->perm.as<uint32_t>(), n, cnt);
+  TJ_CHECK_LAUNCH();
+  ScanScratch sc = scan_scratch(ctx, n, s);
+  scan_exclusive(LoadAt<int64_t>{cnt}, StoreAt<int64_t>{offsets}, n, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  if (total == 0) return;
+
+  ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
+  uint32_t* fill = ctx->fill.as<uint32_t>();
+  TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
+  scatter_pairs_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
+      ctx->pairs.as<uint2>(), total, ctx->perm.as<uint32_t>(), offsets, fill, nbr);
+  TJ_CHECK_LAUNCH();
+
+  // row sorts; `fill` is reused as the list of long rows once the scatter is done
+  unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
+  TJ_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
+  uint32_t* big_rows = fill;  // safe: the scatter kernel finished on this stream
+  sort_rows_warp_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(offsets, n, nbr, big_rows, nbig);
+  TJ_CHECK_LAUNCH();
+  unsigned long long h_nbig = 0;
+  TJ_CUDA(cudaMemcpyAsync(&h_nbig, nbig, sizeof(h_nbig), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  if (h_nbig == 0) return;
+  ctx->vals_alt.ensure(sizeof(uint32_t) * h_nbig, s);
+  uint32_t* huge = ctx->vals_alt.as<uint32_t>();
+  sort_rows_block_kernel<<<unsigned(std::min<unsigned long long>(h_nbig, kNumSMs * 4)), 1024, 0,
+                           s>>>(offsets, nbr, big_rows, nbig, huge, nbig + 1);
+  TJ_CHECK_LAUNCH();
+  unsigned long long h_nhuge = 0;
+  TJ_CUDA(cudaMemcpyAsync(&h_nhuge, nbig + 1, sizeof(h_nhuge), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  if (h_nhuge == 0) return;
+
+  // composite-key radix sort over all huge rows together
+  std::vector<uint32_t> hh(h_nhuge);
+  TJ_CUDA(cudaMemcpyAsync(hh.data(), huge, sizeof(uint32_t) * h_nhuge, cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> hoff(n + 1);
+  TJ_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> hbase(h_nhuge + 1, 0);
+  for (size_t h = 0; h < hh.size(); ++h) {
+    int64_t se[2];
+    TJ_CUDA(cudaMemcpy(se, offsets + hh[h], 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    hbase[h + 1] = hbase[h] + (se[1] - se[0]);
+  }
+  const int64_t m = hbase[h_nhuge];
+  DevBuf kb, kb2, vb, vb2, bb, hb;
+  kb.ensure(sizeof(uint64_t) * m, s);
+  kb2.ensure(sizeof(uint64_t) * m, s);
+  vb.ensure(sizeof(uint32_t) * m, s);
+  vb2.ensure(sizeof(uint32_t) * m, s);
+  bb.ensure(sizeof(int64_t) * (h_nhuge + 1), s);
+  TJ_CUDA(cudaMemcpyAsync(bb.ptr, hbase.data(), sizeof(int64_t) * (h_nhuge + 1),
+                          cudaMemcpyHostToDevice, s));
+  dim3 g(unsigned(std::min<int64_t>(ceil_div(m, 256), 1024)),
+         unsigned(std::min<unsigned long long>(h_nhuge, 65535)));
+  huge_gather_kernel<<<g, 256, 0, s>>>(offsets, nbr, huge, int(h_nhuge), bb.as<int64_t>(),
+                                       kb.as<uint64_t>());
+  TJ_CHECK_LAUNCH();
+  int hbits = 0;
+  while ((1ull << hbits) < h_nhuge) ++hbits;
+  hb.ensure(sizeof(int64_t) * radix_sort_scratch_elems(m), s);
+  ScanScratch sc2 = scan_scratch(ctx, std::max<int64_t>(radix_sort_scratch_elems(m), n), s);
+  int where = radix_sort_pairs(kb.as<uint64_t>(), vb.as<uint32_t>(), kb2.as<uint64_t>(),
+                               vb2.as<uint32_t>(), m, 32 + hbits, true, hb.as<int64_t>(), sc2, s);
+  huge_scatter_kernel<<<g, 256, 0, s>>>(offsets, nbr, huge, int(h_nhuge), bb.as<int64_t>(),
+                                        where ? kb2.as<uint64_t>() : kb.as<uint64_t>());
+  TJ_CHECK_LAUNCH();
+  TJ_CUDA(cudaStreamSynchronize(s));
+  kb.release(s);
+  kb2.release(s);
+  vb.release(s);
+  vb2.release(s);
+  bb.release(s);
+  hb.release(s);
+}
+
+}  // namespace tj

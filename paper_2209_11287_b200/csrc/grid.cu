@@ -1,0 +1,496 @@
+// Device epsilon-grid index: cell keys, radix sort by cell, cell-ordered
+// coordinates + chunk norms, the non-empty cell table, compacted candidate runs
+// and the per-cell estimate.
+//
+// Reference semantics (grid.py):
+//   coords = floor(x[:, :k] / eps) (FP64 true divide, grid.py:81) — here
+//     __ddiv_rn + round-down conversion, bit-identical per coordinate;
+//   stable lexsort, dim 0 primary (grid.py:83) — here a packed key with dim 0
+//     in the high bits and a stable LSD radix sort of (key, id);
+//   cells dict + ordered_cells + point_order (grid.py:85-94) — the sorted run
+//     table (cell_key, cell_start) and perm;
+//   candidates_for_cell = members of the occupied Chebyshev-1 neighbours in
+//     lexicographic order (grid.py:104-133) — every neighbour row that differs
+//     only in the last indexed dim is one contiguous position range of the
+//     cell-ordered array, so a cell's candidate list is <= 3^(k-1) runs found by
+//     two binary searches each, already in the reference's concatenation order.
+#include <climits>
+
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace tj {
+
+struct KeyParams {
+  int k;
+  int shift[TJ_MAX_K_IDX];
+  long long cmin[TJ_MAX_K_IDX];
+};
+
+__device__ __forceinline__ long long cell_coord(double x, double eps) {
+  return __double2ll_rd(__ddiv_rn(x, eps));  // floor(x / eps), IEEE division
+}
+
+__global__ void minmax_init_kernel(long long* mm, int k) {
+  int j = threadIdx.x;
+  if (j < k) {
+    mm[2 * j] = LLONG_MAX;
+    mm[2 * j + 1] = LLONG_MIN;
+  }
+  if (j == 0) mm[2 * TJ_MAX_K_IDX] = 0;  // max squared norm, as bits of a non-negative double
+}
+
+__global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int ld, int k,
+                                   double eps, long long* mm) {
+  long long lo[TJ_MAX_K_IDX], hi[TJ_MAX_K_IDX];
+#pragma unroll
+  for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+    lo[j] = LLONG_MAX;
+    hi[j] = LLONG_MIN;
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+      if (j < k) {
+        long long c = cell_coord(x[i * ld + j], eps);
+        lo[j] = min(lo[j], c);
+        hi[j] = max(hi[j], c);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+    if (j >= k) break;
+    long long a = lo[j], b = hi[j];
+    for (int o = 16; o > 0; o >>= 1) {
+      a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane_id() == 0) {
+      atomicMin(&mm[2 * j], a);
+      atomicMax(&mm[2 * j + 1], b);
+    }
+  }
+}
+
+__global__ void cell_key_kernel(const double* __restrict__ x, int64_t n, int ld, double eps,
+                                KeyParams kp, uint64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t key = 0;
+#pragma unroll
+    for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+      if (j < kp.k) {
+        long long c = cell_coord(x[i * ld + j], eps);
+        key |= uint64_t(c - kp.cmin[j] + 1) << kp.shift[j];
+      }
+    }
+    keys[i] = key;
+  }
+}
+
+// Cell-ordered zero-padded coordinates, chunk norms in the reference order
+// ((((0+x0^2)+x1^2)+x2^2)+x3^2 per chunk, kernels.py:126-130) and full norms.
+__global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, int d, int d_pad,
+                               const uint32_t* __restrict__ perm, double* __restrict__ P,
+                               double* __restrict__ CN, double* __restrict__ NRM,
+                               unsigned long long* max_norm_bits) {
+  const int nchunks = d_pad / 4;
+  unsigned long long local_max = 0;
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t id = perm[p];
+    const double* src = x + id * ld;
+    double* dst = P + p * d_pad;
+    double total = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      double v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = 4 * c + t;
+        v[t] = j < d ? src[j] : 0.0;
+      }
+      double2* dst2 = reinterpret_cast<double2*>(dst + 4 * c);
+      dst2[0] = make_double2(v[0], v[1]);
+      dst2[1] = make_double2(v[2], v[3]);
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s = __dadd_rn(s, __dmul_rn(v[t], v[t]));
+      CN[p * nchunks + c] = s;
+      total = __dadd_rn(total, s);
+    }
+    NRM[p] = total;
+    local_max = max(local_max, (unsigned long long)__double_as_longlong(total));
+  }
+  for (int o = 16; o > 0; o >>= 1)
+    local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if (lane_id() == 0) atomicMax(max_norm_bits, local_max);
+}
+
+struct HeadFlag {
+  const uint64_t* keys;
+  __device__ int64_t operator()(int64_t i) const { return i == 0 || keys[i] != keys[i - 1]; }
+};
+struct CellTableOut {
+  const uint64_t* keys;
+  uint64_t* cell_key;
+  int64_t* cell_start;
+  __device__ void operator()(int64_t i, int64_t excl) const {
+    if (i == 0 || keys[i] != keys[i - 1]) {
+      cell_key[excl] = keys[i];
+      cell_start[excl] = i;
+    }
+  }
+};
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct RowParams {
+  int k;
+  int n_rows;                     // 3^(k-1)
+  long long shift[TJ_MAX_K_IDX];  // as 64-bit for the offset arithmetic
+};
+
+// Position range [b, e) of neighbour row r of the cell with key `key`.
+__device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key, int r,
+                                              const uint64_t* cell_key, const int64_t* cell_start,
+                                              int64_t n_cells, int64_t& b, int64_t& e) {
+  long long delta = 0;
+  int rr = r;
+  for (int j = rp.k - 2; j >= 0; --j) {  // dim k-2 is the fastest-varying digit
+    const int o = rr % 3 - 1;
+    rr /= 3;
+    delta += (long long)o << rp.shift[j];
+  }
+  const uint64_t last = 1ull << rp.shift[rp.k - 1];
+  const uint64_t lo_key = key + uint64_t(delta) - last;
+  const uint64_t hi_key = key + uint64_t(delta) + last;
+  const int64_t a = lower_bound_u64(cell_key, n_cells, lo_key);
+  const int64_t z = upper_bound_u64(cell_key, n_cells, hi_key);
+  b = cell_start[a];
+  e = cell_start[z];
+}
+
+// Warp per cell: number of non-empty runs and candidates.
+__global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
+                                  const int64_t* __restrict__ cell_start, int64_t n_cells,
+                                  int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
+    const uint64_t key = cell_key[c];
+    int64_t runs = 0, cands = 0;
+    for (int r = lane_id(); r < rp.n_rows; r += 32) {
+      int64_t b, e;
+      neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
+      if (e > b) {
+        runs += 1;
+        cands += e - b;
+      }
+    }
+    runs = warp_sum(runs);
+    cands = warp_sum(cands);
+    if (lane_id() == 0) {
+      run_count[c] = runs;
+      cand_count[c] = cands;
+    }
+  }
+}
+
+__global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
+                                 const int64_t* __restrict__ cell_start, int64_t n_cells,
+                                 const int64_t* __restrict__ cell_runs, uint2* __restrict__ runs,
+                                 uint32_t* __restrict__ run_off) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const unsigned lt = lanemask_lt();
+  for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
+    const uint64_t key = cell_key[c];
+    int64_t out = cell_runs[c];
+    int64_t off = 0;  // offset of the next run inside the concatenated candidate list
+    for (int r0 = 0; r0 < rp.n_rows; r0 += 32) {
+      const int r = r0 + lane_id();
+      int64_t b = 0, e = 0;
+      if (r < rp.n_rows) neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
+      const unsigned m = __ballot_sync(0xffffffffu, e > b);
+      const int64_t len = e - b;
+      const int64_t inc = warp_inclusive_scan(len);
+      if (e > b) {
+        runs[out + __popc(m & lt)] = make_uint2(uint32_t(b), uint32_t(e));
+        run_off[out + __popc(m & lt)] = uint32_t(off + inc - len);
+      }
+      out += __popc(m);
+      off += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+}
+
+// cost = |cell|*|cand|, tiles = ceil(|cell|/8)*ceil(|cand|/8) (join.py:170-173, 257-261).
+__global__ void cell_cost_kernel(const int64_t* __restrict__ cell_start,
+                                 const int64_t* __restrict__ cand, int64_t n_cells,
+                                 int64_t* __restrict__ cost, unsigned long long* totals) {
+  unsigned long long c_sum = 0, t_sum = 0, mx = 0;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t nq = cell_start[c + 1] - cell_start[c];
+    const int64_t nc = cand[c];
+    cost[c] = nq * nc;
+    c_sum += nq * nc;
+    t_sum += ((nq + 7) / 8) * ((nc + 7) / 8);
+    mx = max(mx, (unsigned long long)nq);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c_sum += __shfl_xor_sync(0xffffffffu, c_sum, o);
+    t_sum += __shfl_xor_sync(0xffffffffu, t_sum, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane_id() == 0) {
+    atomicAdd(&totals[0], c_sum);
+    atomicAdd(&totals[1], t_sum);
+    atomicMax(&totals[2], mx);
+  }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), kNumSMs * 16)));
+}
+
+ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s) {
+  ctx->scan_partial.ensure(sizeof(int64_t) * (scan_tiles(n) + 1), s);
+  ctx->scan_total.ensure(sizeof(int64_t) * 4, s);
+  return ScanScratch{ctx->scan_partial.as<int64_t>(), ctx->scan_total.as<int64_t>()};
+}
+
+template <class T>
+static T read_scalar(const void* dptr, cudaStream_t s) {
+  T v;
+  TJ_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, int k, double eps,
+                cudaStream_t s) {
+  GridState& g = ctx->g;
+  g = GridState{};
+  g.n = n;
+  g.d = d;
+  g.d_pad = int(ceil_div(d, 4) * 4);
+  g.nchunks = g.d_pad / 4;
+  g.k = k;
+  g.eps = eps;
+  g.eps_sq = eps * eps;  // fl(eps*eps) as in join.py:176
+  const int ld = int(ld64);
+
+  // 1. cell coordinate bounds -> packed key layout
+  ctx->minmax.ensure(sizeof(long long) * (2 * TJ_MAX_K_IDX + 2), s);
+  long long* mm = ctx->minmax.as<long long>();
+  minmax_init_kernel<<<1, 32, 0, s>>>(mm, k);
+  TJ_CHECK_LAUNCH();
+  cell_minmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, k, eps, mm);
+  TJ_CHECK_LAUNCH();
+  long long hmm[2 * TJ_MAX_K_IDX];
+  TJ_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(long long) * 2 * k, cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  int bits[TJ_MAX_K_IDX];
+  int total_bits = 0;
+  for (int j = 0; j < k; ++j) {
+    const unsigned long long span = (unsigned long long)(hmm[2 * j + 1] - hmm[2 * j]) + 2ull;
+    int b = 0;
+    while (b < 64 && (span >> b) != 0) ++b;
+    bits[j] = b;
+    total_bits += b;
+    g.cmin[j] = hmm[2 * j];
+  }
+  if (total_bits > 63)
+    fail(TJ_EINVAL, "cell key over k_idx=" + std::to_string(k) + " indexed dimensions needs " +
+                        std::to_string(total_bits) +
+                        " bits (> 63); use a smaller k_idx or a larger epsilon");
+  int sh = 0;
+  for (int j = k - 1; j >= 0; --j) {
+    g.shift[j] = sh;
+    sh += bits[j];
+  }
+  g.key_bits = total_bits;
+
+  // 2. keys, 3. stable radix sort of (key, id)
+  ctx->keys.ensure(sizeof(uint64_t) * n, s);
+  ctx->keys_alt.ensure(sizeof(uint64_t) * n, s);
+  ctx->perm.ensure(sizeof(uint32_t) * n, s);
+  ctx->vals_alt.ensure(sizeof(uint32_t) * n, s);
+  KeyParams kp{};
+  kp.k = k;
+  for (int j = 0; j < k; ++j) {
+    kp.shift[j] = g.shift[j];
+    kp.cmin[j] = g.cmin[j];
+  }
+  cell_key_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, ctx->keys.as<uint64_t>());
+  TJ_CHECK_LAUNCH();
+  const int64_t hist_elems = radix_sort_scratch_elems(n);
+  ctx->sort_hist.ensure(sizeof(int64_t) * hist_elems, s);
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
+  int where = radix_sort_pairs(ctx->keys.as<uint64_t>(), ctx->perm.as<uint32_t>(),
+                               ctx->keys_alt.as<uint64_t>(), ctx->vals_alt.as<uint32_t>(), n,
+                               total_bits, true, ctx->sort_hist.as<int64_t>(), sc, s);
+  if (where == 1) {
+    std::swap(ctx->keys, ctx->keys_alt);
+    std::swap(ctx->perm, ctx->vals_alt);
+  }
+  const uint64_t* keys = ctx->keys.as<uint64_t>();
+
+  // 4. run table of non-empty cells
+  ctx->cell_key.ensure(sizeof(uint64_t) * (n + 1), s);
+  ctx->cell_start.ensure(sizeof(int64_t) * (n + 1), s);
+  scan_exclusive(HeadFlag{keys},
+                 CellTableOut{keys, ctx->cell_key.as<uint64_t>(), ctx->cell_start.as<int64_t>()},
+                 n, sc, s);
+  g.n_cells = read_scalar<int64_t>(sc.total, s);
+  TJ_CUDA(cudaMemcpyAsync(ctx->cell_start.as<int64_t>() + g.n_cells, &n, sizeof(int64_t),
+                          cudaMemcpyHostToDevice, s));
+
+  // 5. cell-ordered coordinates + norms
+  ctx->P.ensure(sizeof(double) * n * g.d_pad, s);
+  ctx->CN.ensure(sizeof(double) * n * g.nchunks, s);
+  ctx->NRM.ensure(sizeof(double) * n, s);
+  permute_kernel<<<grid_for(n, 256), 256, 0, s>>>(
+      x, n, ld, d, g.d_pad, ctx->perm.as<uint32_t>(), ctx->P.as<double>(), ctx->CN.as<double>(),
+      ctx->NRM.as<double>(), reinterpret_cast<unsigned long long*>(mm + 2 * TJ_MAX_K_IDX));
+  TJ_CHECK_LAUNCH();
+
+  // 6. candidate runs
+  RowParams rp{};
+  rp.k = k;
+  rp.n_rows = 1;
+  for (int j = 0; j < k - 1; ++j) rp.n_rows *= 3;
+  for (int j = 0; j < k; ++j) rp.shift[j] = g.shift[j];
+  const int64_t nc = g.n_cells;
+  ctx->cell_runs.ensure(sizeof(int64_t) * (nc + 1), s);
+  ctx->cell_cand.ensure(sizeof(int64_t) * (nc + 1), s);
+  ctx->cell_cost.ensure(sizeof(int64_t) * (nc + 1), s);
+  ctx->tmp64.ensure(sizeof(int64_t) * (nc + 1), s);
+  const unsigned warp_blocks = grid_for(nc * 32, 256);
+  cand_count_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
+                                                ctx->cell_start.as<int64_t>(), nc,
+                                                ctx->tmp64.as<int64_t>(),
+                                                ctx->cell_cand.as<int64_t>());
+  TJ_CHECK_LAUNCH();
+  sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
+  scan_exclusive(LoadAt<int64_t>{ctx->tmp64.as<int64_t>()},
+                 StoreAt<int64_t>{ctx->cell_runs.as<int64_t>()}, nc, sc, s);
+  g.n_runs = read_scalar<int64_t>(sc.total, s);
+  TJ_CUDA(cudaMemcpyAsync(ctx->cell_runs.as<int64_t>() + nc, &g.n_runs, sizeof(int64_t),
+                          cudaMemcpyHostToDevice, s));
+  ctx->runs.ensure(sizeof(uint2) * std::max<int64_t>(g.n_runs, 1), s);
+  ctx->run_off.ensure(sizeof(uint32_t) * std::max<int64_t>(g.n_runs, 1), s);
+  cand_fill_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
+                                               ctx->cell_start.as<int64_t>(), nc,
+                                               ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+                                               ctx->run_off.as<uint32_t>());
+  TJ_CHECK_LAUNCH();
+
+  // 7. per-cell estimate and totals
+  unsigned long long* totals = reinterpret_cast<unsigned long long*>(ctx->scan_total.as<int64_t>());
+  TJ_CUDA(cudaMemsetAsync(totals, 0, 4 * sizeof(int64_t), s));
+  cell_cost_kernel<<<grid_for(nc, 256), 256, 0, s>>>(ctx->cell_start.as<int64_t>(),
+                                                     ctx->cell_cand.as<int64_t>(), nc,
+                                                     ctx->cell_cost.as<int64_t>(), totals);
+  TJ_CHECK_LAUNCH();
+  unsigned long long ht[3];
+  unsigned long long maxnorm_bits;
+  TJ_CUDA(cudaMemcpyAsync(ht, totals, sizeof(ht), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaMemcpyAsync(&maxnorm_bits, mm + 2 * TJ_MAX_K_IDX, sizeof(maxnorm_bits),
+                          cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  g.candidates = int64_t(ht[0]);
+  g.tiles = int64_t(ht[1]);
+  g.max_cell = int64_t(ht[2]);
+  double mn;
+  memcpy(&mn, &maxnorm_bits, sizeof(mn));
+  g.max_norm = mn;
+  g.built = true;
+}
+
+// ---------------------------------------------------------------- work items
+struct ItemCountIn {
+  const int64_t* cell_start;
+  const int64_t* cand;
+  int64_t cb;
+  int qpi;
+  int64_t target;
+  __device__ int64_t operator()(int64_t i) const {
+    const int64_t c = cb + i;
+    const int64_t nq = cell_start[c + 1] - cell_start[c];
+    const int64_t nc = cand[c];
+    const int64_t qeff = nq < qpi ? nq : qpi;
+    int64_t slice = (target / (qeff > 0 ? qeff : 1) + 7) / 8 * 8;
+    if (slice < 256) slice = 256;
+    const int64_t nqb = (nq + qpi - 1) / qpi;
+    const int64_t nsl = (nc + slice - 1) / slice;
+    return nqb * nsl;
+  }
+};
+
+__global__ void item_fill_kernel(const int64_t* __restrict__ cell_start,
+                                 const int64_t* __restrict__ cand, int64_t cb, int64_t n,
+                                 int qpi, int64_t target, const int64_t* __restrict__ offs,
+                                 WorkItem* __restrict__ items) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = cb + i;
+    const int64_t q_begin = cell_start[c];
+    const int64_t nq = cell_start[c + 1] - q_begin;
+    const int64_t nc = cand[c];
+    const int64_t qeff = nq < qpi ? nq : qpi;
+    int64_t slice = (target / (qeff > 0 ? qeff : 1) + 7) / 8 * 8;
+    if (slice < 256) slice = 256;
+    int64_t o = offs[i];
+    for (int64_t q = 0; q < nq; q += qpi) {
+      for (int64_t s0 = 0; s0 < nc; s0 += slice) {
+        WorkItem w;
+        w.cell = uint32_t(c);
+        w.q0 = uint32_t(q_begin + q);
+        w.nq = uint32_t(min(int64_t(qpi), nq - q));
+        w.s0 = uint32_t(s0);
+        w.s1 = uint32_t(min(nc, s0 + slice));
+        w.pad = 0;
+        items[o++] = w;
+      }
+    }
+  }
+}
+
+int64_t build_work_items(tj_ctx* ctx, int64_t cb, int64_t ce, int qpi, int64_t target,
+                         cudaStream_t s) {
+  const int64_t n = ce - cb;
+  if (n <= 0) return 0;
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+  ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
+  ItemCountIn in{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb, qpi, target};
+  scan_exclusive(in, StoreAt<int64_t>{ctx->tmp64.as<int64_t>()}, n, sc, s);
+  const int64_t total = read_scalar<int64_t>(sc.total, s);
+  ctx->items.ensure(sizeof(WorkItem) * std::max<int64_t>(total, 1), s);
+  item_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(ctx->cell_start.as<int64_t>(),
+                                                    ctx->cell_cand.as<int64_t>(), cb, n, qpi,
+                                                    target, ctx->tmp64.as<int64_t>(),
+                                                    ctx->items.as<WorkItem>());
+  TJ_CHECK_LAUNCH();
+  return total;
+}
+
+}  // namespace tj

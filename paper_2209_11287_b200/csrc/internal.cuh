@@ -1,0 +1,143 @@
+// Library-internal declarations: the context, device buffers, work items and
+// the host-side launchers shared between translation units.
+#pragma once
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tj {
+
+struct ScanScratch;
+
+// Grow-only device buffer on the stream-ordered allocator.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+  void ensure(size_t need, cudaStream_t s) {
+    if (need <= bytes) return;
+    if (ptr) TJ_CUDA(cudaFreeAsync(ptr, s));
+    ptr = nullptr;
+    bytes = 0;
+    size_t want = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMallocAsync(&ptr, want, s);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      ptr = nullptr;
+      fail(TJ_ENOMEM, "device allocation of " + std::to_string(want) + " bytes failed: " +
+                          cudaGetErrorString(e));
+    }
+    bytes = want;
+  }
+  void release(cudaStream_t s) {
+    if (ptr) cudaFreeAsync(ptr, s);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+// One unit of refine work: queries [q0, q0+nq) (cell-ordered positions, all in
+// `cell`) against the candidate slice [s0, s1) of that cell's concatenated
+// candidate list (grid.py:121-133 order).  s0 is a multiple of 8 so 8-candidate
+// tiles line up with the reference's tiling of the concatenation (join.py:261).
+struct WorkItem {
+  uint32_t cell;
+  uint32_t q0;
+  uint32_t nq;
+  uint32_t s0;
+  uint32_t s1;
+  uint32_t pad;
+};
+
+// Device-side counters, one struct per ctx.
+struct DevCounters {
+  unsigned long long pairs;         // appended pairs (keeps counting past capacity)
+  unsigned long long tiles;         // DMMA tiles evaluated
+  unsigned long long chunks_exec;   // DMMA chunks executed
+  unsigned long long chunks_skip;   // DMMA chunks skipped by the short-circuit
+  unsigned long long refined;       // candidate pairs refined
+  unsigned long long rechecks;      // guard-band rechecks
+  unsigned long long item_next;     // persistent-kernel work counter
+  unsigned long long pad;
+};
+
+// Everything a refine kernel needs, passed by value.
+struct RefineArgs {
+  const double* P;         // (n, d_pad) cell-ordered coordinates
+  const double* NRM;       // (n) squared norms (any rounding order; the guard covers it)
+  const double* CN;        // (n, nchunks) chunk norms, reference order (kernels.py:126-130)
+  const uint2* runs;       // (n_runs) candidate position ranges [begin, end)
+  const uint32_t* run_off; // (n_runs) offset of each run inside its cell's concatenation
+  const int64_t* cell_runs;   // (n_cells+1)
+  const int64_t* cell_start;  // (n_cells+1)
+  const WorkItem* items;
+  int64_t n_items;
+  DevCounters* ctr;
+  uint2* pairs;            // append buffer of (query pos, candidate pos)
+  unsigned long long pair_cap;
+  uint32_t* qcount;        // (n) per-query pair counts (cell-ordered positions)
+  int d, d_pad, nchunks;
+  double eps_sq;
+  double guard_rel;        // guard band = guard_rel * (qn + max_norm)
+  double max_norm;
+  int short_circuit;
+};
+
+struct GridState {
+  bool built = false;
+  int64_t n = 0;
+  int d = 0, d_pad = 0, k = 0, nchunks = 0;
+  double eps = 0, eps_sq = 0;
+  int key_bits = 0;
+  int shift[TJ_MAX_K_IDX] = {};
+  int64_t cmin[TJ_MAX_K_IDX] = {};
+  int64_t n_cells = 0, n_runs = 0, candidates = 0, tiles = 0, max_cell = 0;
+  double max_norm = 0;
+};
+
+}  // namespace tj
+
+struct tj_ctx {
+  int device = 0;
+  std::string err;
+  cudaStream_t last_stream = nullptr;
+  tj::GridState g;
+  // grid buffers
+  tj::DevBuf P, NRM, CN, perm, keys, cell_key, cell_start, cell_runs, runs, run_off, cell_cand,
+      cell_cost;
+  // scratch
+  tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
+  // results
+  tj::DevBuf pairs, qcount, counters, fill;
+  unsigned long long pair_cap = 0;
+  int64_t n_items = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool have_refine_timing = false;
+};
+
+namespace tj {
+// sort.cu
+int64_t radix_sort_scratch_elems(int64_t n);
+int radix_sort_pairs(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, int64_t n,
+                     int key_bits, bool identity_values, int64_t* hist, ScanScratch scan,
+                     cudaStream_t stream);
+// grid.cu
+void build_grid(tj_ctx* ctx, const double* coords, int64_t n, int d, int64_t ld, int k,
+                double eps, cudaStream_t s);
+int64_t build_work_items(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, int q_per_item,
+                         int64_t slice, cudaStream_t s);
+ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
+// refine_core.cu / refine_dmma.cu
+void launch_refine_core(const RefineArgs& a, cudaStream_t s);
+void launch_refine_dmma(const RefineArgs& a, cudaStream_t s);
+int core_queries_per_item(int d, int d_pad);
+int dmma_queries_per_item(int d, int d_pad);
+// finalize.cu
+void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t total,
+                  cudaStream_t s);
+}  // namespace tj

@@ -1,0 +1,336 @@
+"""Epsilon self-join on B200: the drop-in for tilejoin.join (join.py:1-349).
+
+`self_join(dataset, JoinConfig(epsilon=...)) -> JoinResult` keeps the
+reference's signature, validation, error types, batching/capacity-guard
+behaviour, counters and canonical (query id, neighbour id) ordering.  The
+work runs on the GPU through libtedjoin.so:
+
+    H2D coords -> tj_build_grid (cell keys, radix sort, cell table, candidate
+    runs, estimates) -> per batch tj_refine (DMMA or CUDA-core FP64 + pair
+    append) -> tj_finalize (CSR by original id, rows sorted) -> D2H CSR.
+
+`kernel="tile"` selects the paper's tensor-core formulation (mma.sync m8n8k4
+f64), `kernel="scalar"` the CUDA-core direct form (GDS-Join style); as in the
+reference, only epsilon changes the pair set.  The pair set is the reference
+direct-form set exactly: the tile path re-decides every pair whose expanded
+value lies inside its rounding guard band with the direct form.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .datasets import Dataset, as_dataset, reorder_dims_by_variance
+from .errors import ResourceError, ValidationError
+
+DEFAULT_K_IDX_CAP = 6  # grid.py:22
+
+
+def default_k_idx(d: int) -> int:
+    return min(d, DEFAULT_K_IDX_CAP)
+
+
+@dataclass(frozen=True)
+class JoinConfig:
+    """Join parameters (join.py:30-46); only epsilon affects which pairs are returned.
+
+    kernel: 'tile' = DMMA tensor-core path, 'scalar' = CUDA-core FP64 path.
+    batch_size: target estimated pairs per batch (None = one batch).
+    k_idx: indexed dimensions, default min(d, 6); the device grid supports <= 8.
+    thread_count: accepted for compatibility (host threading has no role here).
+    device: CUDA device index (extension; None = torch's current device).
+    """
+
+    epsilon: float
+    kernel: str = "tile"
+    short_circuit: bool = True
+    k_idx: int | None = None
+    batch_size: int | None = None
+    thread_count: int = 1
+    reorder_dims: bool = False
+    device: int | None = None
+
+
+@dataclass
+class JoinStats:
+    """Counters and phase timings from one join run (join.py:49-77)."""
+
+    tiles_processed: int = 0
+    chunks_executed: int = 0
+    chunks_skipped: int = 0
+    candidates_refined: int = 0
+    pairs_emitted: int = 0
+    index_seconds: float = 0.0
+    refine_seconds: float = 0.0
+    total_seconds: float = 0.0
+    guard_rechecks: int = 0
+
+    @property
+    def pairs_per_second(self) -> float:
+        return self.pairs_emitted / self.total_seconds if self.total_seconds > 0 else 0.0
+
+    def as_dict(self) -> dict:
+        return {
+            "tiles_processed": self.tiles_processed,
+            "chunks_executed": self.chunks_executed,
+            "chunks_skipped": self.chunks_skipped,
+            "candidates_refined": self.candidates_refined,
+            "pairs_emitted": self.pairs_emitted,
+            "index_seconds": self.index_seconds,
+            "refine_seconds": self.refine_seconds,
+            "total_seconds": self.total_seconds,
+            "pairs_per_second": self.pairs_per_second,
+        }
+
+
+class JoinResult:
+    """Pair set of the join: ordered (query id, neighbour id), self-pairs included.
+
+    The primary form is CSR: ``offsets`` (int64, n+1) and ``neighbors`` (int32,
+    ascending within each row), i.e. per-point neighbour lists.  ``pairs`` is the
+    reference's (m, 2) int64 array sorted by (query, neighbour) (join.py:80-91),
+    materialised on first access.
+    """
+
+    __slots__ = ("offsets", "neighbors", "total_pairs", "selectivity", "stats", "_pairs")
+
+    def __init__(self, offsets, neighbors, total_pairs, selectivity, stats):
+        self.offsets = offsets
+        self.neighbors = neighbors
+        self.total_pairs = int(total_pairs)
+        self.selectivity = float(selectivity)
+        self.stats = stats
+        self._pairs = None
+
+    @property
+    def pairs(self) -> np.ndarray:
+        if self._pairs is None:
+            n = len(self.offsets) - 1
+            counts = np.diff(self.offsets)
+            out = np.empty((self.total_pairs, 2), dtype=np.int64)
+            out[:, 0] = np.repeat(np.arange(n, dtype=np.int64), counts)
+            out[:, 1] = self.neighbors[: self.total_pairs]
+            self._pairs = out
+        return self._pairs
+
+    def neighbors_of(self, i: int) -> np.ndarray:
+        return self.neighbors[self.offsets[i] : self.offsets[i + 1]]
+
+    def __repr__(self) -> str:
+        return f"JoinResult(total_pairs={self.total_pairs}, selectivity={self.selectivity:.4f})"
+
+
+@dataclass(frozen=True)
+class BatchPlan:
+    """Cell ranges (into the lexicographic cell list) per batch (join.py:94-99)."""
+
+    batches: list = field(default_factory=list)
+    estimated_pairs: list = field(default_factory=list)
+
+
+def selectivity(result: JoinResult, n: int) -> float:
+    """Average neighbours per query excluding self: (|R| - n) / n (join.py:102-106)."""
+    if n < 1:
+        raise ValidationError(f"n must be >= 1, got {n}")
+    return (result.total_pairs - n) / n
+
+
+def join_stats(result: JoinResult) -> JoinStats:
+    return result.stats
+
+
+def plan_from_estimates(cell_estimates, batch_size) -> BatchPlan:
+    """Greedy contiguous batches closing once the running estimate reaches batch_size.
+
+    Same partition as _plan_from_estimates (join.py:128-147), computed with a
+    prefix sum + binary search per batch instead of a per-cell Python loop.
+    """
+    if batch_size is not None and batch_size < 1:
+        raise ValidationError(f"batch_size must be >= 1, got {batch_size}")
+    est = np.asarray(cell_estimates, dtype=np.int64)
+    n_cells = len(est)
+    if batch_size is None:
+        return BatchPlan(batches=[(0, n_cells)], estimated_pairs=[int(est.sum())])
+    csum = np.cumsum(est)
+    batches, estimates = [], []
+    start, base = 0, 0
+    while start < n_cells:
+        # first i >= start with csum[i] - base >= batch_size
+        i = int(np.searchsorted(csum, base + batch_size, side="left"))
+        if i >= n_cells:
+            batches.append((start, n_cells))
+            estimates.append(int(csum[-1] - base))
+            break
+        batches.append((start, i + 1))
+        estimates.append(int(csum[i] - base))
+        base = int(csum[i])
+        start = i + 1
+    return BatchPlan(batches=batches, estimated_pairs=estimates)
+
+
+def plan_batches(index, config: JoinConfig) -> BatchPlan:
+    """Batch plan over a built index (join.py:114-125): estimate |cell| * |cand(cell)|."""
+    return plan_from_estimates(index.cell_costs(), config.batch_size)
+
+
+def _validate_config(config: JoinConfig) -> None:
+    """join.py:218-226."""
+    if not np.isfinite(config.epsilon) or config.epsilon <= 0:
+        raise ValidationError(f"epsilon must be positive and finite, got {config.epsilon}")
+    if config.kernel not in ("tile", "scalar"):
+        raise ValidationError(f"kernel must be 'tile' or 'scalar', got {config.kernel!r}")
+    if config.batch_size is not None and config.batch_size < 1:
+        raise ValidationError(f"batch_size must be >= 1, got {config.batch_size}")
+    if config.thread_count < 1:
+        raise ValidationError(f"thread_count must be >= 1, got {config.thread_count}")
+
+
+def resolve_k_idx(config: JoinConfig, d: int) -> int:
+    k_idx = config.k_idx if config.k_idx is not None else default_k_idx(d)
+    if not 1 <= k_idx <= d:  # grid.py:79-80
+        raise ValidationError(f"k_idx must be in [1, {d}], got {k_idx}")
+    if k_idx > _native.TJ_MAX_K_IDX:
+        raise ValidationError(
+            f"k_idx must be <= {_native.TJ_MAX_K_IDX} on the device grid, got {k_idx}")
+    return k_idx
+
+
+def upload(work: Dataset, device: int):
+    """Host Dataset.coords -> device tensor with the same (n, d_padded) layout."""
+    import torch
+
+    host = torch.from_numpy(work.coords)
+    return host.to(device=f"cuda:{device}", non_blocking=False)
+
+
+class DeviceJoin:
+    """The join pipeline on one device, split into the steps bench.py times.
+
+    prepare(): H2D + grid build; refine(): all batches; finalize(): canonical CSR
+    on device; fetch(): D2H.  `self_join` chains them.
+    """
+
+    def __init__(self, work: Dataset, config: JoinConfig, device: int | None = None):
+        import torch
+
+        self.work = work
+        self.config = config
+        self.k_idx = resolve_k_idx(config, work.d)
+        self.ctx = _native.context(device if device is not None else config.device)
+        self.device = self.ctx.device
+        self.kernel = _native.TJ_KERNEL_DMMA if config.kernel == "tile" else _native.TJ_KERNEL_CORE
+        self.torch = torch
+        self.coords = None
+        self.info = None
+        self.total = 0
+
+    def build(self, coords=None):
+        w = self.work
+        self.coords = coords if coords is not None else upload(w, self.device)
+        self.ctx.build_grid(self.coords, w.n, w.d, int(self.coords.stride(0)), self.k_idx,
+                            self.config.epsilon)
+        self.info = self.ctx.grid_info()
+        return self.info
+
+    def plan(self) -> BatchPlan:
+        if self.config.batch_size is None:
+            return BatchPlan(batches=[(0, self.info.n_cells)],
+                             estimated_pairs=[int(self.info.candidates)])
+        return plan_from_estimates(self.ctx.cell_costs(self.info.n_cells), self.config.batch_size)
+
+    def refine(self, cell_range=None, max_result_pairs=None, plan=None):
+        """Run every batch; returns the exact pair count (re-runs once on overflow)."""
+        cfg = self.config
+        if plan is None:
+            plan = self.plan()
+        batches = plan.batches
+        if cell_range is not None:
+            lo, hi = cell_range
+            batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
+        for _attempt in range(2):
+            self.ctx.reset_results()
+            overflowed = False
+            for batch_no, (start, stop) in enumerate(batches):
+                self.ctx.refine(self.kernel, cfg.short_circuit, start, stop)
+                if max_result_pairs is not None:
+                    total, over = self.ctx.result_count()
+                    overflowed |= over
+                    if total > max_result_pairs:  # join.py:198-202
+                        raise ResourceError(
+                            f"batch {batch_no}: result grew to {total} pairs, "
+                            f"beyond the container capacity of {max_result_pairs}")
+                    if over:
+                        break
+            total, over = self.ctx.result_count()
+            if not (over or overflowed):
+                self.total = total
+                return total
+        raise RuntimeError("pair buffer overflowed twice")
+
+    def finalize(self):
+        torch = self.torch
+        n = self.work.n
+        dev = f"cuda:{self.device}"
+        self.offsets_d = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.neighbors_d = torch.empty(max(self.total, 1), dtype=torch.int32, device=dev)
+        self.ctx.finalize(self.offsets_d, self.neighbors_d)
+        return self.offsets_d, self.neighbors_d
+
+    def fetch(self):
+        torch = self.torch
+        off = torch.empty(self.offsets_d.shape, dtype=torch.int64, pin_memory=True)
+        nbr = torch.empty((self.total,), dtype=torch.int32, pin_memory=True)
+        off.copy_(self.offsets_d, non_blocking=True)
+        nbr.copy_(self.neighbors_d[: self.total], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return off.numpy(), nbr.numpy()
+
+    def stats(self) -> JoinStats:
+        st = self.ctx.stats()
+        s = JoinStats(
+            candidates_refined=int(st.candidates_refined),
+            pairs_emitted=int(st.pairs_emitted),
+            guard_rechecks=int(st.guard_rechecks),
+        )
+        if self.config.kernel == "tile":
+            n_chunks = self.work.d_padded // 4
+            if st.tiles_processed or st.candidates_refined == 0:
+                s.tiles_processed = int(st.tiles_processed)
+                s.chunks_executed = int(st.chunks_executed)
+                s.chunks_skipped = int(st.chunks_skipped)
+            else:  # d > 64 or non-finite norms: the exact kernel ran; report the tiling
+                s.tiles_processed = int(self.info.tiles)
+                s.chunks_executed = int(self.info.tiles) * n_chunks
+        return s
+
+
+def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) -> JoinResult:
+    """Find every ordered pair within config.epsilon, self-pairs included (join.py:150-215).
+
+    The pair set depends only on the data and epsilon.  ``max_result_pairs``
+    caps the result and raises ResourceError naming the offending batch.
+    """
+    t_start = time.perf_counter()
+    dataset = as_dataset(dataset)
+    _validate_config(config)
+    work = dataset
+    if config.reorder_dims and dataset.n >= 2:
+        work, _ = reorder_dims_by_variance(dataset)
+    job = DeviceJoin(work, config)
+    job.build()
+    t_indexed = time.perf_counter()
+    total = job.refine(max_result_pairs=max_result_pairs)
+    job.finalize()
+    offsets, neighbors = job.fetch()
+    t_end = time.perf_counter()
+    stats = job.stats()
+    stats.pairs_emitted = total
+    stats.index_seconds = t_indexed - t_start
+    stats.refine_seconds = t_end - t_indexed
+    stats.total_seconds = t_end - t_start
+    return JoinResult(offsets, neighbors, total, (total - dataset.n) / dataset.n, stats)

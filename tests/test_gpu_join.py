@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA self-join through libtedjoin.so vs the oracle and the
+reference's own known answers (test_join.py cases restated, golden fixtures).
+
+The bar is bit-exact pair sets: both kernels decide with the reference direct
+form (the tile path re-decides guard-band pairs), so no epsilon-boundary
+tolerance is needed."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import csr_equal, load_json, sha_pairs
+from paper_2209_11287_b200 import (
+    Dataset,
+    GenSpec,
+    JoinConfig,
+    ResourceError,
+    ValidationError,
+    generate,
+    join_stats,
+    selectivity,
+    self_join,
+)
+from paper_2209_11287_b200 import grid as tgrid
+
+pytestmark = pytest.mark.gpu
+KERNELS = ("tile", "scalar")
+
+
+def assert_oracle_equal(res, ds, eps, k_idx=None):
+    off, nb = oracle.join_csr(ds, eps, k_idx=k_idx)
+    assert res.total_pairs == int(off[-1])
+    assert csr_equal(res.offsets, res.neighbors, off, nb)
+
+
+# --------------------------------------------------------- reference known answers
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_boundary_distance_is_included(kernel):  # test_join.py:29-32
+    r = self_join(Dataset([[0.0, 0.0], [0.25, 0.0]]), JoinConfig(epsilon=0.25, kernel=kernel))
+    assert r.pairs.tolist() == [[0, 0], [0, 1], [1, 0], [1, 1]]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_identical_points_complete_graph(kernel):  # test_join.py:35-40
+    rng = np.random.default_rng(2024)
+    n = 30
+    r = self_join(Dataset(np.tile(rng.random(3), (n, 1))), JoinConfig(epsilon=0.1, kernel=kernel))
+    assert r.total_pairs == n * n
+    assert r.selectivity == n - 1
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_single_point(kernel):  # test_join.py:69-72
+    r = self_join(Dataset([[0.5, 0.5]]), JoinConfig(epsilon=0.1, kernel=kernel))
+    assert r.pairs.tolist() == [[0, 0]]
+    assert r.selectivity == 0.0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_uniform_2d_matches_brute_force(kernel):  # test_join.py:43-49
+    g = load_json("generator.json")
+    ds = generate(GenSpec("uniform", 1000, 2, seed=17))
+    assert ds.checksum() == g["uniform_1000_2_17"]["checksum"]
+    eps = 0.0402  # fixed radius, parity against the restated brute force
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+    truth = oracle.brute_force(ds, eps)
+    assert np.array_equal(r.pairs, truth)
+    assert 5 < r.selectivity < 20
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_self_pairs_and_symmetry(kernel):  # test_join.py:60-66
+    ds = generate(GenSpec("uniform", 300, 4, seed=4))
+    r = self_join(ds, JoinConfig(epsilon=0.3, kernel=kernel))
+    p = r.pairs
+    assert np.all(np.isin(np.arange(300), p[p[:, 0] == p[:, 1], 0]))
+    fwd = set(map(tuple, p.tolist()))
+    assert all((j, i) in fwd for i, j in fwd)
+
+
+def test_selectivity_values():  # test_join.py:219-225
+    r = self_join(Dataset(np.tile([0.1, 0.2], (100, 1))), JoinConfig(epsilon=0.5))
+    assert selectivity(r, 100) == 99.0
+    spread = Dataset(np.column_stack([np.arange(50.0), np.zeros(50)]))
+    assert selectivity(self_join(spread, JoinConfig(epsilon=0.5)), 50) == 0.0
+
+
+def test_capacity_guard_names_the_batch():  # test_join.py:169-172
+    ds = generate(GenSpec("uniform", 300, 2, seed=12))
+    with pytest.raises(ResourceError, match="batch 0"):
+        self_join(ds, JoinConfig(epsilon=0.5), max_result_pairs=10)
+
+
+def test_capacity_guard_later_batch():
+    ds = generate(GenSpec("uniform", 2000, 2, seed=12))
+    full = self_join(ds, JoinConfig(epsilon=0.05))
+    cap = full.total_pairs // 2
+    with pytest.raises(ResourceError, match=r"batch [1-9]"):
+        self_join(ds, JoinConfig(epsilon=0.05, batch_size=500), max_result_pairs=cap)
+
+
+def test_config_validation():  # test_join.py:239-250
+    data = Dataset(np.random.default_rng(0).random((5, 2)))
+    for cfg in (JoinConfig(epsilon=0.0), JoinConfig(epsilon=0.1, kernel="simd"),
+                JoinConfig(epsilon=0.1, batch_size=0), JoinConfig(epsilon=0.1, thread_count=0),
+                JoinConfig(epsilon=0.1, k_idx=7)):
+        with pytest.raises(ValidationError):
+            self_join(data, cfg)
+
+
+# -------------------------------------------------------------- invariances
+
+
+@pytest.fixture(scope="module")
+def case600():
+    ds = generate(GenSpec("uniform", 600, 3, seed=77))
+    eps = 0.0731
+    return ds, eps, self_join(ds, JoinConfig(epsilon=eps))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(short_circuit=False), dict(batch_size=1), dict(batch_size=64), dict(thread_count=4),
+    dict(reorder_dims=True), dict(k_idx=1), dict(k_idx=2), dict(k_idx=3), dict(kernel="scalar"),
+    dict(kernel="scalar", short_circuit=False), dict(kernel="scalar", batch_size=7),
+])
+def test_knobs_do_not_change_pairs(case600, cfg):  # test_join.py:78-127
+    ds, eps, base = case600
+    r = self_join(ds, JoinConfig(epsilon=eps, **cfg))
+    assert np.array_equal(r.pairs, base.pairs)
+    assert_oracle_equal(base, ds, eps)
+
+
+def test_epsilon_monotonicity():  # test_join.py:112-120
+    ds = generate(GenSpec("uniform", 400, 2, seed=31))
+    small = self_join(ds, JoinConfig(epsilon=0.02))
+    large = self_join(ds, JoinConfig(epsilon=0.08))
+    s = set(map(tuple, small.pairs.tolist()))
+    assert s <= set(map(tuple, large.pairs.tolist()))
+
+
+# -------------------------------------------------------------------- stats
+
+
+def test_stats_counters_recount_from_index():  # test_join.py:178-216
+    ds = generate(GenSpec("uniform", 500, 6, seed=13))
+    eps = 0.2
+    r = self_join(ds, JoinConfig(epsilon=eps))
+    _, cstart, _, cand = oracle.grid(ds, eps, 6)
+    nq = np.diff(cstart)
+    tiles = int(np.sum(-(-nq // 8) * -(-cand // 8)))
+    st = join_stats(r)
+    assert st.tiles_processed == tiles
+    assert st.candidates_refined == int(np.sum(nq * cand))
+    assert st.chunks_executed + st.chunks_skipped == tiles * 2
+    assert st.pairs_emitted == r.total_pairs
+    assert st.total_seconds >= st.index_seconds
+
+
+def test_stats_no_short_circuit_means_no_skips():
+    ds = generate(GenSpec("exponential", 400, 8, seed=5))
+    assert self_join(ds, JoinConfig(epsilon=0.02, short_circuit=False)).stats.chunks_skipped == 0
+
+
+def test_short_circuit_skips_chunks():  # test_cli.py:100-117 shape: 300 pts in [0,0.05)^8
+    rng = np.random.default_rng(3)
+    ds = Dataset(rng.random((300, 8)) * 0.05)
+    on = self_join(ds, JoinConfig(epsilon=0.01, short_circuit=True))
+    off = self_join(ds, JoinConfig(epsilon=0.01, short_circuit=False))
+    assert on.stats.chunks_skipped > 0
+    assert np.array_equal(on.pairs, off.pairs)
+
+
+def test_scalar_kernel_reports_no_tiles():  # join.py:328
+    ds = generate(GenSpec("uniform", 200, 3, seed=1))
+    st = self_join(ds, JoinConfig(epsilon=0.2, kernel="scalar")).stats
+    assert st.tiles_processed == 0 and st.chunks_executed == 0
+
+
+# --------------------------------------------------------- golden SPEC sweep
+
+
+def _sweep_cases():
+    try:
+        return load_json("sweep.json")
+    except FileNotFoundError:
+        return []
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{c['dist'][:3]}-n{c['n']}-d{c['d']}-S{c['target']}")
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_spec_sweep_matches_reference(case, kernel):
+    ds = generate(GenSpec(case["dist"], case["n"], case["d"], seed=case["seed"]))
+    assert ds.checksum() == case["checksum"]
+    r = self_join(ds, JoinConfig(epsilon=case["eps"], kernel=kernel))
+    assert r.total_pairs == case["pairs"]
+    assert sha_pairs(r.pairs) == case["sha_pairs"]
+    if kernel == "tile":
+        assert r.stats.tiles_processed == case["tiles"]
+    assert r.stats.candidates_refined == case["candidates"]
+
+
+def test_config1_full_pair_set():
+    c1 = load_json("config1.json")
+    ds = generate(GenSpec("uniform", 100_000, 2, seed=0))
+    assert ds.checksum() == c1["checksum"]
+    for kernel in KERNELS:
+        r = self_join(ds, JoinConfig(epsilon=c1["eps"], kernel=kernel))
+        assert r.total_pairs == c1["scalar"]["pairs"] == 6_502_052
+        assert sha_pairs(r.pairs) == c1["scalar"]["sha_pairs"]
+        assert r.stats.candidates_refined == c1["scalar"]["candidates"]
+
+
+# ------------------------------------------------------------------- grid
+
+
+def test_grid_matches_reference_layout(golden_sweep):
+    for case in golden_sweep[::7]:
+        ds = generate(GenSpec(case["dist"], case["n"], case["d"], seed=case["seed"]))
+        idx = tgrid.build_index(ds, case["eps"])
+        assert idx.n_cells == case["n_cells"]
+        assert sha_pairs(idx.point_order) == case["sha_point_order"]
+        assert sha_pairs(np.asarray(idx.ordered_cells, dtype=np.int64)) == case["sha_cells"]
+        assert sha_pairs(idx.cell_cands) == case["sha_cand_counts"]
+
+
+def test_grid_floor_and_negative_coords():  # test_grid.py:16-37
+    idx = tgrid.build_index(Dataset([[0.05, 0.05], [0.15, 0.05]]), 0.1, 2)
+    assert set(idx.cells) == {(0, 0), (1, 0)}
+    idx = tgrid.build_index(Dataset([[-0.05], [-0.15], [0.05]]), 0.1, 1)
+    assert set(idx.cells) == {(-1,), (-2,), (0,)}
+    idx = tgrid.build_index(Dataset([[1.0], [0.99]]), 0.5, 1)
+    assert idx.cells[(2,)].tolist() == [0] and idx.cells[(1,)].tolist() == [1]
+
+
+def test_grid_candidates_match_oracle():
+    rng = np.random.default_rng(99)
+    for d, k in [(2, 2), (4, 3), (6, 4), (3, 1)]:
+        ds = Dataset(rng.normal(size=(500, d)))
+        eps = 0.35
+        idx = tgrid.build_index(ds, eps, k)
+        order, cstart, ccoord, cand = oracle.grid(ds, eps, k)
+        assert np.array_equal(idx.point_order, order.astype(np.int64))
+        assert [tuple(c) for c in ccoord.tolist()] == idx.ordered_cells
+        assert np.array_equal(idx.cell_cands, cand)
+        for c in idx.ordered_cells[:20]:
+            got = tgrid.neighbor_cells(idx, c)
+            expect = sorted(x for x in idx.cells if max(abs(a - b) for a, b in zip(x, c)) <= 1)
+            assert got == expect
+
+
+# -------------------------------------------------------------- edge cases
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 7, 8, 9, 12, 16, 17, 24, 33, 64])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_dimensionality_ladder(d, kernel):
+    ds = generate(GenSpec("uniform", 1500, d, seed=d))
+    eps = 0.12 * math.sqrt(d)
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+    assert_oracle_equal(r, ds, eps)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_skewed_big_cell_and_long_rows(kernel):
+    """Exponential data: cells far larger than one work item, rows > 256 and > 8192 ids."""
+    ds = generate(GenSpec("exponential", 60_000, 3, seed=3))
+    eps = 0.01
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+    assert_oracle_equal(r, ds, eps)
+    assert np.diff(r.offsets).max() > 8192
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_duplicates_and_exact_shell(kernel):
+    """Coincident points and pairs exactly on the eps shell (guard-band rechecks)."""
+    base = np.array([[0.0, 0.0, 0.0], [0.25, 0.0, 0.0], [0.0, 0.25, 0.0], [0.1, 0.1, 0.1]])
+    pts = np.vstack([base] * 40 + [base + 1.0] * 3)
+    ds = Dataset(pts)
+    r = self_join(ds, JoinConfig(epsilon=0.25, kernel=kernel))
+    assert_oracle_equal(r, ds, 0.25)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_far_from_origin(kernel):
+    """Large coordinates make the expanded form cancel badly: all decisions must still be exact."""
+    rng = np.random.default_rng(5)
+    ds = Dataset(1e4 + rng.random((3000, 4)))
+    eps = 0.09
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+    assert_oracle_equal(r, ds, eps)
+
+
+def test_reference_dataset_object_is_accepted():
+    ds = generate(GenSpec("uniform", 500, 3, seed=2))
+
+    class Foreign:  # duck-typed tilejoin.datasets.Dataset
+        def __init__(self, d):
+            self.coords, self.d, self.n, self.d_padded = d.coords, d.d, d.n, d.d_padded
+
+        @property
+        def logical(self):
+            return self.coords[:, : self.d]
+
+    r1 = self_join(Foreign(ds), JoinConfig(epsilon=0.1))
+    r2 = self_join(ds.logical.copy(), JoinConfig(epsilon=0.1))
+    assert np.array_equal(r1.pairs, r2.pairs)
