@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FP64 epsilon self-join (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--kernel tile]
+    python bench.py --impl reference ...      # the reference path on the host cores
+
+One step = one complete self-join of the configured workload: grid index
+build, estimator/batching, refine (DMMA or CUDA-core FP64) with pair
+emission, canonical CSR output.  `value` is algorithmic FP64 distance
+TFLOP/s = 2*d*C / step time (C = candidate pairs the grid produces, the
+reference's JoinStats.candidates_refined) with inputs resident in HBM; the
+step time in seconds is `ms_per_step`/1000 ("self-join s").  `e2e` repeats
+the measurement through the public API `self_join(host Dataset, JoinConfig)`
+with H2D of the coordinates and D2H of the CSR pair set inside the timed
+region.  N>1 ranks (torchrun) broadcast the dataset over NCCL and split the
+cells by estimated cost; times are the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "self-join s & FP64 dist TFLOP/s (frac of peak), TC vs CUDA-core, 1/2/4/8 B200"
+CONFIGS = {  # BASELINE.md §2 / SURVEY.md §8(d); eps for ~64 neighbours per point
+    "c1": ("uniform", 100_000, 2, 0.0143667),
+    "c2": ("uniform", 2_000_000, 4, 0.051306),
+    "c3": ("exponential", 5_000_000, 8, 0.0118508),
+    "c4d2": ("uniform", 2_000_000, 2, 0.00320714),
+    "c4d4": ("uniform", 2_000_000, 4, 0.051306),
+    "c4d8": ("uniform", 2_000_000, 8, 0.244686),
+    "c4d16": ("uniform", 2_000_000, 16, 0.657508),
+    "c4d32": ("uniform", 2_000_000, 32, 1.31923),
+    "c4d64": ("uniform", 2_000_000, 64, 2.27218),
+    "c5": ("uniform", 50_000_000, 4, 0.0232204),
+}
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- helpers
+def host_info() -> dict:
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": model, "cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def traffic_from_profiles(config: str, kernel: str):
+    """DRAM bytes per refine launch from the committed ncu --set full summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        data = json.loads(p.read_text())
+        return data.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------- CPU side
+def cpu_reference(ds, eps: float, d: int, info_candidates: int, costs, budget_s: float = 20.0,
+                  seed: int = 0) -> dict:
+    """Reference direct-form self-join (oracle C port, all host threads) on a bounded sample."""
+    import oracle
+
+    threads = oracle.num_threads()
+    n_cells = len(costs)
+    total = int(costs.sum())
+    # probe rate on a small seeded sample of cells
+    rng = np.random.default_rng(seed)
+    probe = np.sort(rng.choice(n_cells, size=min(n_cells, 2000), replace=False))
+    t = time.perf_counter()
+    oracle.join_csr(ds, eps, cells=probe, threads=threads)
+    t_probe = time.perf_counter() - t
+    rate = max(int(costs[probe].sum()), 1) / max(t_probe, 1e-6)
+    if total / rate <= budget_s:
+        cells, label = None, "full workload"
+        c_sample = total
+    else:
+        want = rate * budget_s * 0.75
+        top = np.argsort(-costs, kind="stable")[:10]
+        order = rng.permutation(n_cells)
+        pick, acc = list(top), int(costs[top].sum())
+        for c in order:
+            if acc >= want:
+                break
+            if c in pick:
+                continue
+            pick.append(int(c))
+            acc += int(costs[c])
+        cells = np.sort(np.asarray(pick, dtype=np.int64))
+        c_sample = int(costs[cells].sum())
+        label = f"{len(cells)} of {n_cells} cells (10 costliest + seeded random), {c_sample} of {total} candidate pairs"
+    t = time.perf_counter()
+    oracle.join_csr(ds, eps, cells=cells, threads=threads)
+    secs = time.perf_counter() - t
+    return {"value": 2.0 * d * c_sample / secs / 1e12, "unit": "TFLOP/s", "cores": threads,
+            "kind": "port", "sample": label, "seconds": secs,
+            "candidate_pairs_per_s": c_sample / secs,
+            "extrapolated_full_join_s": secs * total / max(c_sample, 1)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm (oracle C port of grid.py + join.py scalar
+    refinement) on the host cores, rank 0 only."""
+    dist_name, n, d, eps = CONFIGS[args.config]
+    if rank != 0:
+        return
+    import oracle
+    from paper_2209_11287_b200.datasets import GenSpec, generate
+
+    ds = generate(GenSpec(dist_name, n, d, seed=0))
+    order, cstart, ccoord, cand = oracle.grid(ds, eps, min(d, 6))
+    costs = np.diff(cstart) * cand
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(ds, eps, d, int(costs.sum()), costs, budget_s=args.cpu_budget / max(args.steps, 1), seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    secs = float(np.median([r["extrapolated_full_join_s"] for r in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seed 0)",
+        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps},
+        "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "TFLOP/s"},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU side
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2209_11287_b200 import _native
+    from paper_2209_11287_b200.datasets import Dataset, GenSpec, generate
+    from paper_2209_11287_b200.distributed import balanced_cell_ranges, broadcast_dataset
+    from paper_2209_11287_b200.join import DeviceJoin, JoinConfig, self_join
+
+    dist_name, n, d, eps = CONFIGS[args.config]
+    dev = local
+    torch.cuda.set_device(dev)
+    ds = generate(GenSpec(dist_name, n, d, seed=0)) if rank == 0 else None
+    cfg = JoinConfig(epsilon=eps, kernel=args.kernel, short_circuit=not args.no_short_circuit,
+                     device=dev)
+    # device-resident input on rank 0; other ranks receive it inside the step
+    coords0 = torch.from_numpy(ds.coords).to(f"cuda:{dev}") if rank == 0 else None
+    dp = 4 * ((d + 3) // 4)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(kernel_cfg, timings=None):
+        import torch.distributed as dist
+
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        if world > 1:
+            coords = coords0 if rank == 0 else torch.empty((n, dp), dtype=torch.float64,
+                                                            device=f"cuda:{dev}")
+            dist.broadcast(coords, src=0)
+        else:
+            coords = coords0
+        ev[1].record(stream)
+        # non-root ranks hold only the shape on the host (np.empty touches no pages)
+        work = ds if ds is not None else Dataset._wrap(np.empty((n, dp)), d)
+        job = DeviceJoin(work, kernel_cfg, device=dev)
+        info = job.build(coords)
+        ev[2].record(stream)
+        cell_range = None
+        if world > 1:
+            costs = job.ctx.cell_costs(info.n_cells)
+            cell_range = balanced_cell_ranges(costs, world)[rank]
+        job.refine(cell_range=cell_range)
+        refine_ms = job.ctx.last_refine_ms()
+        ev[3].record(stream)
+        job.finalize()
+        ev[4].record(stream)
+        torch.cuda.synchronize(dev)
+        st = job.ctx.stats()
+        if timings is not None:
+            timings.append({
+                "step_ms": ev[0].elapsed_time(ev[4]),
+                "bcast_ms": ev[0].elapsed_time(ev[1]),
+                "index_ms": ev[1].elapsed_time(ev[2]),
+                "refine_ms": ev[2].elapsed_time(ev[3]),
+                "refine_kernel_ms": refine_ms,
+                "finalize_ms": ev[3].elapsed_time(ev[4]),
+                "candidates": int(info.candidates),
+                "rank_candidates": int(st.candidates_refined),
+                "pairs": int(job.total),
+                "n_cells": int(info.n_cells),
+                "rechecks": int(st.guard_rechecks),
+            })
+        return job
+
+    def measure(kernel_cfg, steps, warmup):
+        for _ in range(warmup):
+            one_step(kernel_cfg)
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        timings = []
+        launches0 = _native.launch_count()
+        with ClockSampler(dev) as clk:
+            torch.cuda.synchronize(dev)
+            barrier(world)
+            for _ in range(steps):
+                one_step(kernel_cfg, timings)
+                flush.zero_()  # L2 flush between steps, outside the step events
+            torch.cuda.synchronize(dev)
+            barrier(world)
+        launches = _native.launch_count() - launches0
+        return timings, clk.summary(), launches
+
+    timings, clocks, launches = measure(cfg, args.steps, args.warmup)
+    step_ms = max_over_ranks(float(np.mean([t["step_ms"] for t in timings])), world)
+    C = timings[0]["candidates"]
+    value = 2.0 * d * C / (step_ms * 1e-3) / 1e12
+
+    # TC vs CUDA-core: the other kernel on the same harness
+    other = "scalar" if args.kernel == "tile" else "tile"
+    ocfg = JoinConfig(epsilon=eps, kernel=other, short_circuit=cfg.short_circuit, device=dev)
+    o_t, _, _ = measure(ocfg, max(1, min(args.steps, 3)), 1)
+    o_step = max_over_ranks(float(np.mean([t["step_ms"] for t in o_t])), world)
+    o_ref = max_over_ranks(float(np.mean([t["refine_kernel_ms"] for t in o_t])), world)
+
+    # roofline of the dominant kernel (refine), FP64 peak measured in-run
+    peak_dmma, _ = _native.fp64_peak(1)
+    peak_dfma, _ = _native.fp64_peak(0)
+    peak = max(peak_dmma, peak_dfma)
+    ref_ms = float(np.mean([t["refine_kernel_ms"] for t in timings]))
+    rank_c = timings[0]["rank_candidates"]
+    achieved = 2.0 * d * rank_c / (ref_ms * 1e-3) / 1e12
+    share = ref_ms / float(np.mean([t["step_ms"] for t in timings]))
+
+    # e2e through the public API with host buffers
+    e2e_val = None
+    h2d = n * dp * 8
+    d2h = (n + 1) * 8 + timings[0]["pairs"] * 4
+    if world == 1:
+        for _ in range(max(1, args.warmup - 1)):
+            self_join(ds, cfg)
+        ts = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            r = self_join(ds, cfg)
+            ts.append(time.perf_counter() - t)
+        e2e_s = float(np.mean(ts))
+        d2h = (n + 1) * 8 + r.total_pairs * 4
+        e2e_val = 2.0 * d * C / e2e_s / 1e12
+    else:
+        from paper_2209_11287_b200.distributed import shard_self_join
+
+        ts = []
+        for i in range(args.warmup + args.steps):
+            barrier(world)
+            t = time.perf_counter()
+            shard_self_join(ds, cfg)
+            el = max_over_ranks(time.perf_counter() - t, world)
+            if i >= args.warmup:
+                ts.append(el)
+        e2e_s = float(np.mean(ts))
+        e2e_val = 2.0 * d * C / e2e_s / 1e12
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.skip_cpu:
+        import oracle
+
+        order, cstart, ccoord, cand = oracle.grid(ds, eps, min(d, 6))
+        costs = np.diff(cstart) * cand
+        cpu = cpu_reference(ds, eps, d, C, costs, budget_s=args.cpu_budget)
+    mean = lambda k: float(np.mean([t[k] for t in timings]))
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "self_join_s": step_ms / 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)",
+        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps,
+                   "kernel": args.kernel, "short_circuit": cfg.short_circuit,
+                   "candidate_pairs": C, "result_pairs": timings[0]["pairs"],
+                   "n_cells": timings[0]["n_cells"], "l2": "256 MiB write between steps",
+                   "parallelism": f"cells split by estimated cost over {world} rank(s)"},
+        "phases_ms": {k: mean(k) for k in ("bcast_ms", "index_ms", "refine_ms", "refine_kernel_ms",
+                                           "finalize_ms")},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic_from_profiles(args.config, args.kernel),
+                     "kernel": "refine_dmma_kernel" if args.kernel == "tile" else "refine_core_kernel",
+                     "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, DFMA {peak_dfma:.2f}) TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
+                     "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))",
+                     "share_of_step": share},
+        "tc_vs_core": {args.kernel: {"step_ms": step_ms, "refine_kernel_ms": ref_ms,
+                                     "refine_tflops": achieved},
+                       other: {"step_ms": o_step, "refine_kernel_ms": o_ref,
+                               "refine_tflops": 2.0 * d * rank_c / (o_ref * 1e-3) / 1e12}},
+        "e2e": {"value": e2e_val, "unit": "TFLOP/s", "seconds": e2e_s,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "self_join(host Dataset, JoinConfig) -> CSR in pinned host memory"
+                       if world == 1 else "distributed.shard_self_join (NCCL bcast, gloo gather)"},
+        "gpu_launches": launches,
+        "guard_rechecks": timings[0]["rechecks"],
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--kernel", choices=("tile", "scalar"), default="tile")
+    ap.add_argument("--no-short-circuit", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

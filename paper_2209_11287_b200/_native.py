@@ -59,6 +59,7 @@ SIGNATURES = {
     "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
     "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_last_refine_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
+    "tj_launch_count": (_i64, []),
 }
 
 _lib = None
@@ -210,6 +211,11 @@ def context(device: int | None = None) -> Context:
         if ctx is None:
             ctx = _contexts[dev] = Context(dev)
         return ctx
+
+
+def launch_count() -> int:
+    """Kernels libtedjoin.so has launched in this process."""
+    return int(load_library().tj_launch_count())
 
 
 def fp64_peak(kind: int, iters: int = 8192) -> tuple[float, float]:

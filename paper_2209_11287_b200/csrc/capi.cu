@@ -1,6 +1,7 @@
 // extern "C" entry points of libtedjoin.so (declared in include/tedjoin.h).
 // Every entry point converts internal failures into a status code and keeps
 // the message for tj_last_error(); no C++ exception crosses the ABI.
+#include <atomic>
 #include <cmath>
 #include <mutex>
 
@@ -10,6 +11,9 @@
 namespace tj {
 
 [[noreturn]] void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static std::mutex g_err_mu;
 static std::string g_err;  // failures without a ctx (tj_ctx_create)
@@ -71,6 +75,8 @@ using namespace tj;
 extern "C" {
 
 int tj_version(void) { return 100; }
+
+int64_t tj_launch_count(void) { return g_launches.load(); }
 
 int tj_ctx_create(int device, tj_ctx** out) {
   if (!out) return TJ_EINVAL;

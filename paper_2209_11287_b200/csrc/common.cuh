@@ -29,7 +29,14 @@ struct Error {
                                " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
 
-#define TJ_CHECK_LAUNCH() TJ_CUDA(cudaGetLastError())
+// Every kernel launch of the library goes through TJ_CHECK_LAUNCH, which also
+// counts it (tj_launch_count: the bench's gpu_launches evidence).
+void note_launch();
+#define TJ_CHECK_LAUNCH()          \
+  do {                             \
+    ::tj::note_launch();           \
+    TJ_CUDA(cudaGetLastError());   \
+  } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
