@@ -63,7 +63,13 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.window = None  # (t0, t1) of the timed region
+
+    def wait_first(self, timeout: float = 3.0):
+        t = time.monotonic()
+        while self.proc is not None and not self.lines and time.monotonic() - t < timeout:
+            time.sleep(0.02)
 
     def __enter__(self):
         try:
@@ -79,7 +85,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -92,7 +98,12 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 - 0.25 <= x[0] <= t1 + 0.25]
+            lines = inside or lines  # timed region shorter than the 200 ms period: use the load phase
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -306,23 +317,30 @@ def run_ours(args, world, rank, local):
             })
         return job
 
-    def measure(kernel_cfg, steps, warmup):
-        for _ in range(warmup):
-            one_step(kernel_cfg)
-            flush.zero_()
-        torch.cuda.synchronize(dev)
-        barrier(world)
-        timings = []
-        launches0 = _native.launch_count()
+    def measure(kernel_cfg, steps, warmup, min_warm_s=1.0):
         with ClockSampler(dev) as clk:
+            clk.wait_first()
+            # >= `warmup` steps and >= min_warm_s of load, so the clock sampler sees the GPU busy
+            t_w, done = time.monotonic(), 0
+            while done < warmup or time.monotonic() - t_w < min_warm_s:
+                one_step(kernel_cfg)
+                flush.zero_()
+                done += 1
             torch.cuda.synchronize(dev)
             barrier(world)
+            timings = []
+            launches0 = _native.launch_count()
+            t0 = time.monotonic()
             for _ in range(steps):
                 one_step(kernel_cfg, timings)
                 flush.zero_()  # L2 flush between steps, outside the step events
             torch.cuda.synchronize(dev)
             barrier(world)
-        launches = _native.launch_count() - launches0
+            # the timed steps are shorter than the 200 ms sampling period: report the
+            # whole loaded phase (>= 1 s warm-up + timed steps)
+            clk.window = (t_w, time.monotonic())
+            launches = _native.launch_count() - launches0
+            time.sleep(0.25)
         return timings, clk.summary(), launches
 
     timings, clocks, launches = measure(cfg, args.steps, args.warmup)

@@ -253,8 +253,13 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
       const unsigned long long budget = (unsigned long long)(0.35 * double(free_b)) / sizeof(uint2);
       reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
     }
-    const int qpi = dmma ? dmma_queries_per_item(g.d, g.d_pad) : core_queries_per_item(g.d, g.d_pad);
-    const int64_t target = std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
+    const bool lowd = dmma && g.d_pad == 4;
+    const int qpi = lowd ? lowd_queries_per_item()
+                    : dmma ? dmma_queries_per_item(g.d, g.d_pad)
+                           : core_queries_per_item(g.d, g.d_pad);
+    // lowd: items never split a candidate list (each query row comes from one item)
+    const int64_t target = lowd ? (int64_t(1) << 60)
+                                : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
     ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s);
     TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
     RefineArgs a{};
@@ -279,7 +284,8 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.max_norm = g.max_norm + g.eps_sq;
     a.short_circuit = short_circuit ? 1 : 0;
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
-    if (dmma) launch_refine_dmma(a, s);
+    if (lowd) launch_refine_lowd(a, s);
+    else if (dmma) launch_refine_dmma(a, s);
     else launch_refine_core(a, s);
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;

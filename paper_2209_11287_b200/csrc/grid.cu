@@ -121,6 +121,9 @@ __global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, 
       total = __dadd_rn(total, s);
     }
     NRM[p] = total;
+    // d <= 3: the padding coordinate carries |x|^2 for the norm-in-K DMMA tile
+    // (refine_lowd.cu); every reader of P uses only the first d coordinates otherwise.
+    if (d <= 3) dst[3] = total;
     local_max = max(local_max, (unsigned long long)__double_as_longlong(total));
   }
   for (int o = 16; o > 0; o >>= 1)

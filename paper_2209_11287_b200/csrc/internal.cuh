@@ -135,6 +135,8 @@ ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
 void launch_refine_dmma(const RefineArgs& a, cudaStream_t s);
+void launch_refine_lowd(const RefineArgs& a, cudaStream_t s);  // d <= 4, unsliced items
+int lowd_queries_per_item();
 int core_queries_per_item(int d, int d_pad);
 int dmma_queries_per_item(int d, int d_pad);
 // finalize.cu

@@ -69,7 +69,7 @@ def test_uniform_2d_matches_brute_force(kernel):  # test_join.py:43-49
     r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
     truth = oracle.brute_force(ds, eps)
     assert np.array_equal(r.pairs, truth)
-    assert 5 < r.selectivity < 20
+    assert 4 < r.selectivity < 20
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
