@@ -369,8 +369,12 @@ def run_ours(args, world, rank, local):
     h2d = n * dp * 8
     d2h = (n + 1) * 8 + timings[0]["pairs"] * 4
     if world == 1:
-        for _ in range(max(1, args.warmup - 1)):
-            self_join(ds, cfg)
+        # warm-up keeps the previous result alive like the timed loop does, so the
+        # pinned host buffers of two results are cached (no cudaHostAlloc when timed)
+        prev = None
+        for _ in range(max(2, args.warmup)):
+            prev = self_join(ds, cfg)
+        r = prev
         ts = []
         for _ in range(args.steps):
             flush.zero_()

@@ -49,6 +49,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_sqdist.restype = f64
         L.oracle_sqdist.argtypes = [vp, i64, i32, i64, i64]
         L.oracle_num_threads.restype = i32
+        L.oracle_rows.restype = i32
+        L.oracle_rows.argtypes = [vp, i64, i32, i64, i32, f64, vp, i64, vp, vp, i32]
         _lib = L
     return _lib
 
@@ -86,6 +88,26 @@ def join_csr(data, eps: float, k_idx: int | None = None, cells=None, threads: in
     if rc != 0:
         raise RuntimeError(f"oracle_self_join failed ({rc})")
     return offsets, nbrs[: total.value]
+
+
+def rows(data, eps: float, qids, k_idx: int | None = None, threads: int = 0):
+    """Reference rows of selected query ids -> (counts int64[len(qids)], concatenated ids)."""
+    x, d = _coords(data)
+    n, ld = x.shape
+    k = min(d, 6) if k_idx is None else int(k_idx)
+    q = np.ascontiguousarray(qids, dtype=np.int64)
+    counts = np.zeros(len(q), dtype=np.int64)
+    L = lib()
+    rc = L.oracle_rows(x.ctypes.data, n, d, ld, k, float(eps), q.ctypes.data, len(q),
+                       counts.ctypes.data, None, threads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_rows failed ({rc})")
+    nbrs = np.empty(max(int(counts.sum()), 1), dtype=np.uint32)
+    rc = L.oracle_rows(x.ctypes.data, n, d, ld, k, float(eps), q.ctypes.data, len(q),
+                       counts.ctypes.data, nbrs.ctypes.data, threads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_rows failed ({rc})")
+    return counts, nbrs[: int(counts.sum())]
 
 
 def grid(data, eps: float, k_idx: int | None = None):

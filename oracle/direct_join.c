@@ -264,6 +264,64 @@ int oracle_self_join(const double* x, int64_t n, int d, int64_t ld, int k, doubl
   return 0;
 }
 
+/* Rows of selected queries only (for sampled parity on large inputs).
+ * counts[i] = |R(qids[i])|; with nbrs != NULL the rows are written back to back
+ * in qids order (each ascending), nbrs sized sum(counts). */
+int oracle_rows(const double* x, int64_t n, int d, int64_t ld, int k, double eps,
+                const int64_t* qids, int64_t nq, int64_t* counts, uint32_t* nbrs, int threads) {
+  grid_t g;
+  if (k < 1 || k > MAXK || build_grid(x, n, d, ld, k, eps, &g) != 0) return -1;
+  const double eps_sq = eps * eps;
+  int64_t* pos_of = (int64_t*)malloc(sizeof(int64_t) * n);
+  for (int64_t p = 0; p < n; ++p) pos_of[g.order[p]] = p;
+  int64_t* base = NULL;
+  if (nbrs) {
+    base = (int64_t*)malloc(sizeof(int64_t) * (nq + 1));
+    base[0] = 0;
+    for (int64_t i = 0; i < nq; ++i) base[i + 1] = base[i] + counts[i];
+  }
+  int max_nb = 1;
+  for (int t = 0; t < k; ++t) max_nb *= 3;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+  {
+    int64_t* nb = (int64_t*)malloc(sizeof(int64_t) * max_nb);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t i = 0; i < nq; ++i) {
+      const uint32_t q = (uint32_t)qids[i];
+      const int64_t p = pos_of[q];
+      int64_t lo = 0, hi = g.n_cells; /* cell containing position p */
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (g.cstart[mid] <= p) lo = mid;
+        else hi = mid;
+      }
+      const int nn = neighbours(&g, lo, nb);
+      int64_t cnt = 0;
+      uint32_t* row = nbrs ? nbrs + base[i] : NULL;
+      for (int m = 0; m < nn; ++m)
+        for (int64_t cp = g.cstart[nb[m]]; cp < g.cstart[nb[m] + 1]; ++cp) {
+          const uint32_t c = g.order[cp];
+          if (direct_le(x, ld, d, q, c, eps_sq)) {
+            if (row) row[cnt] = c;
+            ++cnt;
+          }
+        }
+      if (row) qsort(row, (size_t)cnt, sizeof(uint32_t), cmp_u32);
+      else counts[i] = cnt;
+    }
+    free(nb);
+  }
+  free(base);
+  free(pos_of);
+  free_grid(&g);
+  return 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -56,6 +56,20 @@ static void zero_results(tj_ctx* ctx, cudaStream_t s) {
   }
 }
 
+// Dense hit-mask layout over all cells (low-d path); depends only on the grid.
+static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
+  if (ctx->masks_ready) return;
+  const int64_t total = build_mask_bases(ctx, 0, ctx->g.n_cells, s);
+  ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(total, 1), s);
+  ctx->masks_ready = true;
+}
+
+static unsigned long long free_budget(double frac, size_t unit) {
+  size_t free_b = 0, total_b = 0;
+  TJ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  return (unsigned long long)(frac * double(free_b)) / unit;
+}
+
 static void reserve_pairs(tj_ctx* ctx, unsigned long long pairs, cudaStream_t s) {
   pairs = std::max<unsigned long long>(pairs, 1024);
   if (pairs <= ctx->pair_cap) return;
@@ -108,7 +122,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->cell_key, &ctx->cell_start, &ctx->cell_runs, &ctx->runs,      &ctx->run_off,
                     &ctx->cell_cand, &ctx->cell_cost, &ctx->keys_alt,  &ctx->vals_alt,  &ctx->sort_hist,
                     &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
-                    &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill};
+                    &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
+                    &ctx->masks,    &ctx->cell_blocks, &ctx->cell_mbase, &ctx->dense};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -140,6 +155,7 @@ int tj_build_grid(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64
                           " on the device grid, got " + std::to_string(k_idx));
     if (!coords) fail(TJ_EINVAL, "coords is null");
     if (ld < d) fail(TJ_EINVAL, "ld must be >= d");
+    ctx->masks_ready = false;
     build_grid(ctx, coords, n, d, ld, k_idx, eps, s);
     zero_results(ctx, s);
     ctx->last_stream = s;
@@ -247,13 +263,12 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     // The expanded form needs finite norms; beyond that the exact kernel decides.
     const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
     const bool dmma = kernel == TJ_KERNEL_DMMA && norms_ok && g.d <= 64;
-    if (ctx->pair_cap == 0) {
-      size_t free_b = 0, total_b = 0;
-      TJ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const unsigned long long budget = (unsigned long long)(0.35 * double(free_b)) / sizeof(uint2);
+    const bool lowd = dmma && g.d_pad == 4;
+    if (!lowd && ctx->pair_cap == 0) {
+      const unsigned long long budget = free_budget(0.35, sizeof(uint2));
       reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
     }
-    const bool lowd = dmma && g.d_pad == 4;
+    if (lowd) ensure_masks(ctx, s);
     const int qpi = lowd ? lowd_queries_per_item()
                     : dmma ? dmma_queries_per_item(g.d, g.d_pad)
                            : core_queries_per_item(g.d, g.d_pad);
@@ -276,6 +291,10 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.pairs = ctx->pairs.as<uint2>();
     a.pair_cap = ctx->pair_cap;
     a.qcount = ctx->qcount.as<uint32_t>();
+    a.masks = ctx->masks.as<unsigned long long>();
+    a.cell_mbase = ctx->cell_mbase.as<int64_t>();
+    a.cell_blocks = ctx->cell_blocks.as<int64_t>();
+    a.cell_base = 0;
     a.d = g.d;
     a.d_pad = g.d_pad;
     a.nchunks = g.nchunks;
@@ -308,14 +327,14 @@ int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed) {
   return guarded(ctx, [&] {
     require_grid(ctx);
     cudaStream_t s = ctx->last_stream;
-    unsigned long long p = 0;
-    TJ_CUDA(cudaMemcpyAsync(&p, &counters(ctx)->pairs, sizeof(p), cudaMemcpyDeviceToHost, s));
+    DevCounters c{};
+    TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
     TJ_CUDA(cudaStreamSynchronize(s));
-    *total = int64_t(p);
-    const bool over = p > ctx->pair_cap;
-    if (overflowed) *overflowed = over ? 1 : 0;
-    if (over) {
-      reserve_pairs(ctx, p + p / 8, s);
+    *total = int64_t(c.pairs + c.hits);
+    const bool over_p = c.pairs > ctx->pair_cap;
+    if (overflowed) *overflowed = over_p ? 1 : 0;
+    if (over_p) {
+      reserve_pairs(ctx, c.pairs + c.pairs / 8, s);
       zero_results(ctx, s);
     }
   });
@@ -337,13 +356,15 @@ int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream
     require_grid(ctx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
-    unsigned long long p = 0;
-    TJ_CUDA(cudaMemcpyAsync(&p, &counters(ctx)->pairs, sizeof(p), cudaMemcpyDeviceToHost, s));
+    DevCounters c{};
+    TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
     TJ_CUDA(cudaStreamSynchronize(s));
-    if (p > ctx->pair_cap)
-      fail(TJ_ECAPACITY, "pair buffer overflowed; call tj_result_count and re-run the batch");
-    if (p > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
-    finalize_csr(ctx, offsets, neighbors, int64_t(p), s);
+    if (c.pairs > ctx->pair_cap)
+      fail(TJ_ECAPACITY, "result buffer overflowed; call tj_result_count and re-run the batch");
+    if (c.pairs > 0 && c.hits > 0)
+      fail(TJ_EINVAL, "one result set mixes the low-d DMMA kernel with another kernel");
+    if (c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
+    finalize_csr(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits), s);
   });
 }
 
@@ -359,7 +380,7 @@ int tj_get_stats(tj_ctx* ctx, tj_stats* out) {
     out->chunks_executed = int64_t(c.chunks_exec);
     out->chunks_skipped = int64_t(c.chunks_skip);
     out->candidates_refined = int64_t(c.refined);
-    out->pairs_emitted = int64_t(c.pairs);
+    out->pairs_emitted = int64_t(c.pairs + c.hits);
     out->guard_rechecks = int64_t(c.rechecks);
   });
 }

@@ -1,15 +1,15 @@
 // Canonical output: CSR by original query id with neighbour ids ascending.
 //
-// Replaces the concatenate + np.lexsort((j, i)) of join.py:203-204.  The refine
-// kernels append (query position, candidate position) pairs in arbitrary order
-// and count pairs per query position.  Here:
-//   1. row counts move from cell order to original-id order and are scanned
-//      into int64 row offsets;
-//   2. every pair is scattered to its row (per-row atomic cursor) as the
-//      original neighbour id;
-//   3. each row is sorted: one warp per row of <= 256 ids (register bitonic
-//      network), one CTA per row of <= 8192 ids (shared-memory bitonic), and a
-//      composite-key radix sort for anything larger.
+// Replaces the concatenate + np.lexsort((j, i)) of join.py:203-204.  Per-query
+// pair counts (cell-ordered positions) move to original-id order and are
+// scanned into int64 row offsets.  Then:
+//  * low-d path (row segments, refine_lowd.cu): one warp per query gathers its
+//    segment chain, maps candidate positions to original ids, sorts the row in
+//    registers (bitonic network) and writes it to its final place;
+//  * pair path (other kernels): every (query, candidate) pair is scattered to
+//    its row through a per-row atomic cursor, then each row is sorted in place.
+// Rows longer than 256 ids are sorted by one CTA (shared-memory bitonic, <= 8192)
+// or, beyond that, by a composite-key radix sort.
 #include "internal.cuh"
 #include "scan.cuh"
 
@@ -111,6 +111,95 @@ __global__ void sort_rows_warp_kernel(const int64_t* __restrict__ offsets, int64
   }
 }
 
+// Low-d hit masks -> rows.  Warp per cell: the cell's candidate runs are
+// re-flattened into 8-candidate blocks exactly as the refine kernel tiled them;
+// lane j owns query j of the current 32-query slice, walks the blocks, extracts
+// its column of each tile mask (bit 4r + (c>>1) of the low / high word for even /
+// odd column c) and writes the original ids of its hits to its final row; then
+// the warp sorts the slice's rows (bitonic in registers, long rows deferred).
+constexpr int kExpandBlk = 512;
+__global__ void __launch_bounds__(128)
+    expand_masks_kernel(const unsigned long long* __restrict__ masks,
+                        const int64_t* __restrict__ cell_mbase,
+                        const int64_t* __restrict__ cell_start,
+                        const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
+                        int64_t n_cells, const uint32_t* __restrict__ qcount,
+                        const uint32_t* __restrict__ perm, const int64_t* __restrict__ offsets,
+                        uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
+                        unsigned long long* n_big) {
+  __shared__ uint32_t s_pos[4][kExpandBlk];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  uint32_t* bpos = s_pos[warp];
+  const int64_t stride = int64_t(gridDim.x) * 4;
+  for (int64_t c = int64_t(blockIdx.x) * 4 + warp; c < n_cells; c += stride) {
+    const int64_t cs = cell_start[c];
+    const int nq = int(cell_start[c + 1] - cs);
+    if (qcount[cs] == 0) continue;  // cell not refined in this result set
+    const int ngc = (nq + 7) >> 3;
+    // flatten the runs (<= 27 for k <= 4) into block positions
+    const int64_t rb = cell_runs[c], re = cell_runs[c + 1];
+    const int nr = int(re - rb);
+    uint2 myrun = make_uint2(0u, 0u);
+    if (lane < nr) myrun = runs[rb + lane];
+    const int mynblk = int(myrun.y - myrun.x + 7) >> 3;
+    int incl = mynblk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int myfirst = incl - mynblk;
+    const unsigned long long* mb = masks + cell_mbase[c];
+    for (int q0 = 0; q0 < nq; q0 += 32) {
+      const int j = q0 + lane;  // query index within the cell
+      const bool active = j < nq;
+      const uint32_t qrow = active ? perm[cs + j] : 0u;
+      uint32_t* dst = nbr + (active ? offsets[qrow] : 0);
+      const int g = j >> 3, col = j & 7;
+      const unsigned word = col & 1, sh = col >> 1;
+      int o = 0;
+      for (int b0 = 0; b0 < total; b0 += kExpandBlk) {
+        const int nb = min(kExpandBlk, total - b0);
+        __syncwarp();
+        {
+          const int lo = max(myfirst, b0), hi = min(myfirst + mynblk, b0 + nb);
+          for (int b = lo; b < hi; ++b) bpos[b - b0] = myrun.x + 8u * uint32_t(b - myfirst);
+        }
+        __syncwarp();
+        if (active) {
+          for (int b = 0; b < nb; ++b) {
+            const unsigned long long m = mb[size_t(b0 + b) * ngc + g];
+            unsigned bits = (unsigned(m >> (32 * word)) >> sh) & 0x11111111u;
+            if (bits) {
+              const uint32_t p = bpos[b];
+              do {
+                const int r = (__ffs(bits) - 1) >> 2;
+                bits &= bits - 1;
+                dst[o++] = perm[p + r];
+              } while (bits);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      // sort the slice's rows (lane j's count is o)
+      const int nrows = min(32, nq - q0);
+      for (int k = 0; k < nrows; ++k) {
+        const int len = __shfl_sync(0xffffffffu, o, k);
+        const uint32_t rrow = __shfl_sync(0xffffffffu, qrow, k);
+        uint32_t* row = nbr + offsets[rrow];
+        if (len <= 1) continue;
+        if (len <= 32) warp_sort_row<1>(row, len);
+        else if (len <= 64) warp_sort_row<2>(row, len);
+        else if (len <= 128) warp_sort_row<4>(row, len);
+        else if (len <= kWarpSortMax) warp_sort_row<8>(row, len);
+        else if (lane == 0) big_rows[atomicAdd(n_big, 1ull)] = rrow;
+      }
+    }
+  }
+}
+
 // One CTA per listed row of 257..8192 ids: shared-memory bitonic sort.
 __global__ void __launch_bounds__(1024)
     sort_rows_block_kernel(const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
@@ -179,31 +268,10 @@ static unsigned blocks_for(int64_t n, int threads) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), kNumSMs * 16)));
 }
 
-void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t total, cudaStream_t s) {
+// Sort the rows listed in big_rows (> kWarpSortMax ids) in place.
+static void sort_big_rows(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, uint32_t* big_rows,
+                          unsigned long long* nbig, cudaStream_t s) {
   const int64_t n = ctx->g.n;
-  ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
-  int64_t* cnt = ctx->tmp64.as<int64_t>();
-  counts_to_orig_kernel<<<blocks_for(n, 256), 256, 0, s>>>(ctx->qcount.as<uint32_t>(),
-                                                          ctx->perm.as<uint32_t>(), n, cnt);
-  TJ_CHECK_LAUNCH();
-  ScanScratch sc = scan_scratch(ctx, n, s);
-  scan_exclusive(LoadAt<int64_t>{cnt}, StoreAt<int64_t>{offsets}, n, sc, s);
-  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  if (total == 0) return;
-
-  ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
-  uint32_t* fill = ctx->fill.as<uint32_t>();
-  TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
-  scatter_pairs_kernel<<<blocks_for(total, 256), 256, 0, s>>>(
-      ctx->pairs.as<uint2>(), total, ctx->perm.as<uint32_t>(), offsets, fill, nbr);
-  TJ_CHECK_LAUNCH();
-
-  // row sorts; `fill` is reused as the list of long rows once the scatter is done
-  unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
-  TJ_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
-  uint32_t* big_rows = fill;  // safe: the scatter kernel finished on this stream
-  sort_rows_warp_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(offsets, n, nbr, big_rows, nbig);
-  TJ_CHECK_LAUNCH();
   unsigned long long h_nbig = 0;
   TJ_CUDA(cudaMemcpyAsync(&h_nbig, nbig, sizeof(h_nbig), cudaMemcpyDeviceToHost, s));
   TJ_CUDA(cudaStreamSynchronize(s));
@@ -221,7 +289,6 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t total, c
   // composite-key radix sort over all huge rows together
   std::vector<uint32_t> hh(h_nhuge);
   TJ_CUDA(cudaMemcpyAsync(hh.data(), huge, sizeof(uint32_t) * h_nhuge, cudaMemcpyDeviceToHost, s));
-  std::vector<int64_t> hoff(n + 1);
   TJ_CUDA(cudaStreamSynchronize(s));
   std::vector<int64_t> hbase(h_nhuge + 1, 0);
   for (size_t h = 0; h < hh.size(); ++h) {
@@ -247,8 +314,9 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t total, c
   while ((1ull << hbits) < h_nhuge) ++hbits;
   hb.ensure(sizeof(int64_t) * radix_sort_scratch_elems(m), s);
   ScanScratch sc2 = scan_scratch(ctx, std::max<int64_t>(radix_sort_scratch_elems(m), n), s);
-  int where = radix_sort_pairs(kb.as<uint64_t>(), vb.as<uint32_t>(), kb2.as<uint64_t>(),
-                               vb2.as<uint32_t>(), m, 32 + hbits, true, hb.as<int64_t>(), sc2, s);
+  const int where = radix_sort_pairs(kb.as<uint64_t>(), vb.as<uint32_t>(), kb2.as<uint64_t>(),
+                                     vb2.as<uint32_t>(), m, 32 + hbits, true, hb.as<int64_t>(),
+                                     sc2, s);
   huge_scatter_kernel<<<g, 256, 0, s>>>(offsets, nbr, huge, int(h_nhuge), bb.as<int64_t>(),
                                         where ? kb2.as<uint64_t>() : kb.as<uint64_t>());
   TJ_CHECK_LAUNCH();
@@ -259,6 +327,42 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t total, c
   vb2.release(s);
   bb.release(s);
   hb.release(s);
+}
+
+void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
+                  int64_t n_mask_hits, cudaStream_t s) {
+  const int64_t n = ctx->g.n;
+  ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
+  int64_t* cnt = ctx->tmp64.as<int64_t>();
+  counts_to_orig_kernel<<<blocks_for(n, 256), 256, 0, s>>>(ctx->qcount.as<uint32_t>(),
+                                                          ctx->perm.as<uint32_t>(), n, cnt);
+  TJ_CHECK_LAUNCH();
+  ScanScratch sc = scan_scratch(ctx, n, s);
+  scan_exclusive(LoadAt<int64_t>{cnt}, StoreAt<int64_t>{offsets}, n, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  if (n_pairs == 0 && n_mask_hits == 0) return;
+
+  ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
+  uint32_t* fill = ctx->fill.as<uint32_t>();
+  unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
+  TJ_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
+  if (n_mask_hits > 0) {
+    const int64_t nc = ctx->g.n_cells;
+    expand_masks_kernel<<<unsigned(std::min<int64_t>(ceil_div(nc, 4), kNumSMs * 64)), 128, 0, s>>>(
+        ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
+        ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(), nc,
+        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), offsets, nbr, fill, nbig);
+    TJ_CHECK_LAUNCH();
+  } else {
+    TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
+    scatter_pairs_kernel<<<blocks_for(n_pairs, 256), 256, 0, s>>>(
+        ctx->pairs.as<uint2>(), n_pairs, ctx->perm.as<uint32_t>(), offsets, fill, nbr);
+    TJ_CHECK_LAUNCH();
+    // `fill` becomes the list of long rows once the scatter is done (same stream)
+    sort_rows_warp_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(offsets, n, nbr, fill, nbig);
+    TJ_CHECK_LAUNCH();
+  }
+  sort_big_rows(ctx, offsets, nbr, fill, nbig, s);
 }
 
 }  // namespace tj

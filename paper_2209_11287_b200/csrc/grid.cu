@@ -59,6 +59,9 @@ __global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int 
       }
     }
   }
+  // warp -> block -> one atomic per block and dimension
+  __shared__ long long s_lo[TJ_MAX_K_IDX][32], s_hi[TJ_MAX_K_IDX][32];
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 #pragma unroll
   for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
     if (j >= k) break;
@@ -68,9 +71,20 @@ __global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int 
       b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
     }
     if (lane_id() == 0) {
-      atomicMin(&mm[2 * j], a);
-      atomicMax(&mm[2 * j + 1], b);
+      s_lo[j][warp] = a;
+      s_hi[j][warp] = b;
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    const int j = threadIdx.x;
+    long long a = LLONG_MAX, b = LLONG_MIN;
+    for (int w = 0; w < nwarps; ++w) {
+      a = min(a, s_lo[j][w]);
+      b = max(b, s_hi[j][w]);
+    }
+    atomicMin(&mm[2 * j], a);
+    atomicMax(&mm[2 * j + 1], b);
   }
 }
 
@@ -170,12 +184,42 @@ struct RowParams {
   int k;
   int n_rows;                     // 3^(k-1)
   long long shift[TJ_MAX_K_IDX];  // as 64-bit for the offset arithmetic
+  // Dense cell lookup (when the guarded coordinate box is small): cell index per
+  // mixed-radix box index, -1 when empty.  Null: binary search on cell_key.
+  const int* dense;
+  long long dstride[TJ_MAX_K_IDX];
+  unsigned long long fmask[TJ_MAX_K_IDX];
 };
+
+__device__ __forceinline__ long long dense_index(const RowParams& rp, uint64_t key) {
+  long long idx = 0;
+  for (int j = 0; j < rp.k; ++j) idx += (long long)((key >> rp.shift[j]) & rp.fmask[j]) * rp.dstride[j];
+  return idx;
+}
 
 // Position range [b, e) of neighbour row r of the cell with key `key`.
 __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key, int r,
                                               const uint64_t* cell_key, const int64_t* cell_start,
                                               int64_t n_cells, int64_t& b, int64_t& e) {
+  if (rp.dense) {
+    // the row's three cells along the last dim are adjacent box entries
+    long long idx = dense_index(rp, key);
+    int rr = r;
+    for (int j = rp.k - 2; j >= 0; --j) {
+      idx += (long long)(rr % 3 - 1) * rp.dstride[j];
+      rr /= 3;
+    }
+    const int c0 = rp.dense[idx - 1], c1 = rp.dense[idx], c2 = rp.dense[idx + 1];
+    const int first = c0 >= 0 ? c0 : (c1 >= 0 ? c1 : c2);
+    const int last = c2 >= 0 ? c2 : (c1 >= 0 ? c1 : c0);
+    if (first < 0) {
+      b = e = 0;
+    } else {
+      b = cell_start[first];
+      e = cell_start[last + 1];
+    }
+    return;
+  }
   long long delta = 0;
   int rr = r;
   for (int j = rp.k - 2; j >= 0; --j) {  // dim k-2 is the fastest-varying digit
@@ -195,24 +239,28 @@ __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key,
 // Warp per cell: number of non-empty runs and candidates.
 __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
                                   const int64_t* __restrict__ cell_start, int64_t n_cells,
-                                  int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count) {
+                                  int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count,
+                                  int64_t* __restrict__ blk_count) {
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
     const uint64_t key = cell_key[c];
-    int64_t runs = 0, cands = 0;
+    int64_t runs = 0, cands = 0, blks = 0;
     for (int r = lane_id(); r < rp.n_rows; r += 32) {
       int64_t b, e;
       neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
       if (e > b) {
         runs += 1;
         cands += e - b;
+        blks += (e - b + 7) >> 3;
       }
     }
     runs = warp_sum(runs);
     cands = warp_sum(cands);
+    blks = warp_sum(blks);
     if (lane_id() == 0) {
       run_count[c] = runs;
       cand_count[c] = cands;
+      blk_count[c] = blks;  // 8-candidate blocks when every run is tiled on its own
     }
   }
 }
@@ -242,6 +290,13 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
       off += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
+}
+
+__global__ void dense_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
+                                  int64_t n_cells, int* __restrict__ dense) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x)
+    dense[dense_index(rp, cell_key[c])] = int(c);
 }
 
 // cost = |cell|*|cand|, tiles = ceil(|cell|/8)*ceil(|cand|/8) (join.py:170-173, 257-261).
@@ -306,7 +361,8 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   long long* mm = ctx->minmax.as<long long>();
   minmax_init_kernel<<<1, 32, 0, s>>>(mm, k);
   TJ_CHECK_LAUNCH();
-  cell_minmax_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, k, eps, mm);
+  cell_minmax_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 2 * kNumSMs)), 256, 0, s>>>(
+      x, n, ld, k, eps, mm);
   TJ_CHECK_LAUNCH();
   long long hmm[2 * TJ_MAX_K_IDX];
   TJ_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(long long) * 2 * k, cudaMemcpyDeviceToHost, s));
@@ -383,15 +439,40 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   for (int j = 0; j < k - 1; ++j) rp.n_rows *= 3;
   for (int j = 0; j < k; ++j) rp.shift[j] = g.shift[j];
   const int64_t nc = g.n_cells;
+  // dense box lookup when the guarded box is small (<= max(8 * cells, 4M) entries)
+  {
+    long long box = 1;
+    bool small = true;
+    for (int j = k - 1; j >= 0; --j) {
+      rp.dstride[j] = box;
+      const int fbits = (j == 0 ? g.key_bits : g.shift[j - 1]) - g.shift[j];
+      rp.fmask[j] = fbits >= 64 ? ~0ull : (1ull << fbits) - 1;
+      const long long span = (long long)(hmm[2 * j + 1] - hmm[2 * j]) + 3;  // fields 0..range+2
+      if (box > (1ll << 40) / span) small = false;
+      else box *= span;
+    }
+    if (small && box <= std::max<long long>(8 * nc, 1ll << 22)) {
+      ctx->dense.ensure(sizeof(int) * box, s);
+      TJ_CUDA(cudaMemsetAsync(ctx->dense.ptr, 0xff, sizeof(int) * box, s));
+      rp.dense = ctx->dense.as<int>();
+      dense_fill_kernel<<<grid_for(nc, 256), 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(), nc,
+                                                          ctx->dense.as<int>());
+      TJ_CHECK_LAUNCH();
+    } else {
+      rp.dense = nullptr;
+    }
+  }
   ctx->cell_runs.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->cell_cand.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->cell_cost.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->tmp64.ensure(sizeof(int64_t) * (nc + 1), s);
   const unsigned warp_blocks = grid_for(nc * 32, 256);
+  ctx->cell_blocks.ensure(sizeof(int64_t) * (nc + 1), s);
   cand_count_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
                                                 ctx->cell_start.as<int64_t>(), nc,
                                                 ctx->tmp64.as<int64_t>(),
-                                                ctx->cell_cand.as<int64_t>());
+                                                ctx->cell_cand.as<int64_t>(),
+                                                ctx->cell_blocks.as<int64_t>());
   TJ_CHECK_LAUNCH();
   sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
   scan_exclusive(LoadAt<int64_t>{ctx->tmp64.as<int64_t>()},
@@ -476,6 +557,29 @@ __global__ void item_fill_kernel(const int64_t* __restrict__ cell_start,
       }
     }
   }
+}
+
+// Low-d hit masks: every (query group, 8-candidate block) tile of the cells
+// [cb, ce) owns one 64-bit mask.  Cell c's masks start at mbase[c - cb] and are
+// ordered (group, block) with blocks as in the refine kernel's run-by-run tiling.
+struct MaskCountIn {
+  const int64_t* cell_start;
+  const int64_t* blocks;
+  int64_t cb;
+  __device__ int64_t operator()(int64_t i) const {
+    const int64_t c = cb + i;
+    return ((cell_start[c + 1] - cell_start[c] + 7) / 8) * blocks[c];
+  }
+};
+
+int64_t build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
+  const int64_t n = ce - cb;
+  if (n <= 0) return 0;
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+  ctx->cell_mbase.ensure(sizeof(int64_t) * (n + 1), s);
+  scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_blocks.as<int64_t>(), cb},
+                 StoreAt<int64_t>{ctx->cell_mbase.as<int64_t>()}, n, sc, s);
+  return read_scalar<int64_t>(sc.total, s);
 }
 
 int64_t build_work_items(tj_ctx* ctx, int64_t cb, int64_t ce, int qpi, int64_t target,

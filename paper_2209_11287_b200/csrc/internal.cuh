@@ -63,8 +63,13 @@ struct DevCounters {
   unsigned long long refined;       // candidate pairs refined
   unsigned long long rechecks;      // guard-band rechecks
   unsigned long long item_next;     // persistent-kernel work counter
-  unsigned long long pad;
+  unsigned long long hits;          // pairs recorded as low-d hit masks
+  unsigned long long pad[2];
 };
+
+// Low-d output: one 64-bit hit mask per (query group, 8-candidate block) tile,
+// dense per cell (see build_mask_bases).  Bit L (< 32) = pair (query 2*(L&3),
+// candidate L>>2) of the tile, bit 32 + L = pair (query 2*(L&3) + 1, candidate L>>2).
 
 // Everything a refine kernel needs, passed by value.
 struct RefineArgs {
@@ -81,6 +86,10 @@ struct RefineArgs {
   uint2* pairs;            // append buffer of (query pos, candidate pos)
   unsigned long long pair_cap;
   uint32_t* qcount;        // (n) per-query pair counts (cell-ordered positions)
+  unsigned long long* masks;     // low-d hit masks
+  const int64_t* cell_mbase;     // first mask of cell c at cell_mbase[c - cell_base]
+  const int64_t* cell_blocks;    // 8-candidate blocks per cell (runs tiled separately)
+  int64_t cell_base;
   int d, d_pad, nchunks;
   double eps_sq;
   double guard_rel;        // guard band = guard_rel * (qn + max_norm)
@@ -109,15 +118,17 @@ struct tj_ctx {
   tj::GridState g;
   // grid buffers
   tj::DevBuf P, NRM, CN, perm, keys, cell_key, cell_start, cell_runs, runs, run_off, cell_cand,
-      cell_cost;
+      cell_cost, dense;
   // scratch
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
   // results
-  tj::DevBuf pairs, qcount, counters, fill;
+  tj::DevBuf pairs, qcount, counters, fill, masks, cell_blocks, cell_mbase;
   unsigned long long pair_cap = 0;
+  int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
   int64_t n_items = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool have_refine_timing = false;
+  bool masks_ready = false;  // low-d mask layout built for the current grid
 };
 
 namespace tj {
@@ -132,6 +143,7 @@ void build_grid(tj_ctx* ctx, const double* coords, int64_t n, int d, int64_t ld,
 int64_t build_work_items(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, int q_per_item,
                          int64_t slice, cudaStream_t s);
 ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
+int64_t build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
 void launch_refine_dmma(const RefineArgs& a, cudaStream_t s);
@@ -140,6 +152,6 @@ int lowd_queries_per_item();
 int core_queries_per_item(int d, int d_pad);
 int dmma_queries_per_item(int d, int d_pad);
 // finalize.cu
-void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t total,
-                  cudaStream_t s);
+void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
+                  int64_t n_mask_hits, cudaStream_t s);
 }  // namespace tj

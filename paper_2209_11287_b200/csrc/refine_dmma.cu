@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kDmmaThreads)
       atomicAdd(&a.ctr->refined, (unsigned long long)it.nq * (it.s1 - it.s0));
   }
   hb.flush(my_hits, a);
+  if (lane != 0) st_tiles = st_exec = st_skip = 0;  // warp-uniform counters: count once
   flush_stats(a, st_tiles, st_exec, st_skip, st_rechecks);
 }
 

@@ -214,6 +214,41 @@ def test_config1_full_pair_set():
         assert r.stats.candidates_refined == c1["scalar"]["candidates"]
 
 
+def _sampled():
+    try:
+        return load_json("sampled.json")
+    except FileNotFoundError:
+        return []
+
+
+@pytest.mark.parametrize("meta", _sampled(), ids=lambda m: m["config"])
+def test_full_size_configs_match_reference_rows(meta):
+    """Benchmark-size inputs: rows of queries sampled from the 10 costliest cells plus
+    random cells, as computed by the reference's own refiner (tests/golden)."""
+    arr = np.load(oracle.HERE.parent / "tests" / "golden" / "sampled.npz")
+    name = meta["config"]
+    ds = generate(GenSpec(meta["dist"], meta["n"], meta["d"], seed=0))
+    assert ds.checksum() == meta["checksum"]
+    r = self_join(ds, JoinConfig(epsilon=meta["eps"]))
+    q, cnt, nbrs = arr[f"{name}_qids"], arr[f"{name}_counts"], arr[f"{name}_nbrs"]
+    pos = 0
+    for qq, c in zip(q, cnt):
+        row = r.neighbors_of(int(qq)).astype(np.int64)
+        assert len(row) == c, (name, int(qq))
+        assert np.array_equal(row, nbrs[pos: pos + c]), (name, int(qq))
+        pos += c
+    # size-independent invariants of the whole pair set: self-pairs, sorted rows,
+    # symmetry through a checksum of (i, j) vs (j, i) sums
+    counts = np.diff(r.offsets)
+    assert (counts >= 1).all()
+    rows = np.repeat(np.arange(len(counts), dtype=np.int64), counts)
+    nb = r.neighbors.astype(np.int64)
+    assert (np.diff(nb)[np.diff(rows) == 0] > 0).all()
+    h1 = np.bitwise_xor.reduce(rows * 1_000_003 + nb * 7919)
+    h2 = np.bitwise_xor.reduce(nb * 1_000_003 + rows * 7919)
+    assert h1 == h2
+
+
 # ------------------------------------------------------------------- grid
 
 
@@ -268,7 +303,7 @@ def test_dimensionality_ladder(d, kernel):
 def test_skewed_big_cell_and_long_rows(kernel):
     """Exponential data: cells far larger than one work item, rows > 256 and > 8192 ids."""
     ds = generate(GenSpec("exponential", 60_000, 3, seed=3))
-    eps = 0.01
+    eps = 0.016
     r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
     assert_oracle_equal(r, ds, eps)
     assert np.diff(r.offsets).max() > 8192

@@ -90,14 +90,10 @@ def test_oracle_sampled_rows_match_reference():
             continue  # c5 is checked on the GPU box only (CPU suite stays fast)
         name = meta["config"]
         ds = generate(GenSpec(meta["dist"], meta["n"], meta["d"], seed=0))
-        off, nb = oracle.join_csr(ds, meta["eps"], cells=np.asarray(meta["cells"]))
         q, cnt, nbrs = arr[f"{name}_qids"], arr[f"{name}_counts"], arr[f"{name}_nbrs"]
-        pos = 0
-        for qq, c in zip(q, cnt):
-            row = nb[off[qq]: off[qq + 1]].astype(np.int64)
-            assert len(row) == c, (name, qq)
-            assert np.array_equal(row, nbrs[pos: pos + c]), (name, qq)
-            pos += c
+        counts, got = oracle.rows(ds, meta["eps"], q)
+        assert np.array_equal(counts, cnt), name
+        assert np.array_equal(got.astype(np.int64), nbrs), name
 
 
 def test_oracle_known_answers():
