@@ -270,7 +270,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     }
     if (lowd) ensure_masks(ctx, s);
     const int qpi = lowd ? lowd_queries_per_item()
-                    : dmma ? dmma_queries_per_item(g.d, g.d_pad)
+                    : dmma ? tc_queries_per_item(g.d_pad)
                            : core_queries_per_item(g.d, g.d_pad);
     // lowd: items never split a candidate list (each query row comes from one item)
     const int64_t target = lowd ? (int64_t(1) << 60)
@@ -281,6 +281,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.P = ctx->P.as<double>();
     a.NRM = ctx->NRM.as<double>();
     a.CN = ctx->CN.as<double>();
+    a.SFX = ctx->SFX.as<double>();
     a.runs = ctx->runs.as<uint2>();
     a.run_off = ctx->run_off.as<uint32_t>();
     a.cell_runs = ctx->cell_runs.as<int64_t>();
@@ -304,7 +305,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.short_circuit = short_circuit ? 1 : 0;
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
     if (lowd) launch_refine_lowd(a, s);
-    else if (dmma) launch_refine_dmma(a, s);
+    else if (dmma) launch_refine_tc(a, s);
     else launch_refine_core(a, s);
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;

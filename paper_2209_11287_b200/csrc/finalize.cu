@@ -117,8 +117,31 @@ __global__ void sort_rows_warp_kernel(const int64_t* __restrict__ offsets, int64
 // its column of each tile mask (bit 4r + (c>>1) of the low / high word for even /
 // odd column c) and writes the original ids of its hits to its final row; then
 // the warp sorts the slice's rows (bitonic in registers, long rows deferred).
-constexpr int kExpandBlk = 512;
-__global__ void __launch_bounds__(128)
+// Rows of the slice are built in a per-warp shared-memory pool and sorted from
+// there (one coalesced store per row); masks and the original ids of each
+// block's candidates are staged in shared memory first, so the per-hit work is
+// shared-memory only.
+constexpr int kExpandBlk = 64;  // blocks staged per chunk
+constexpr int kExpandPool = 1536;
+constexpr int kExpandWarps = 4;
+
+template <int R>
+__device__ __forceinline__ void sort_store_row(const uint32_t* src, int len, uint32_t* dst) {
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane_id();
+    v[r] = i < len ? src[i] : 0xffffffffu;
+  }
+  warp_bitonic<R>(v);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane_id();
+    if (i < len) dst[i] = v[r];
+  }
+}
+
+__global__ void __launch_bounds__(kExpandWarps * 32)
     expand_masks_kernel(const unsigned long long* __restrict__ masks,
                         const int64_t* __restrict__ cell_mbase,
                         const int64_t* __restrict__ cell_start,
@@ -126,17 +149,23 @@ __global__ void __launch_bounds__(128)
                         int64_t n_cells, const uint32_t* __restrict__ qcount,
                         const uint32_t* __restrict__ perm, const int64_t* __restrict__ offsets,
                         uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
-                        unsigned long long* n_big) {
-  __shared__ uint32_t s_pos[4][kExpandBlk];
+                        unsigned long long* n_big, uint32_t n_points) {
+  __shared__ uint32_t s_pos[kExpandWarps][kExpandBlk];
+  __shared__ uint32_t s_ids[kExpandWarps][kExpandBlk * 8];
+  __shared__ unsigned long long s_msk[kExpandWarps][kExpandBlk * 4];
+  __shared__ uint32_t s_pool[kExpandWarps][kExpandPool];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   uint32_t* bpos = s_pos[warp];
-  const int64_t stride = int64_t(gridDim.x) * 4;
-  for (int64_t c = int64_t(blockIdx.x) * 4 + warp; c < n_cells; c += stride) {
+  uint32_t* bids = s_ids[warp];
+  unsigned long long* bmsk = s_msk[warp];
+  uint32_t* pool = s_pool[warp];
+  const int64_t stride = int64_t(gridDim.x) * kExpandWarps;
+  for (int64_t c = int64_t(blockIdx.x) * kExpandWarps + warp; c < n_cells; c += stride) {
     const int64_t cs = cell_start[c];
     const int nq = int(cell_start[c + 1] - cs);
     if (qcount[cs] == 0) continue;  // cell not refined in this result set
     const int ngc = (nq + 7) >> 3;
-    // flatten the runs (<= 27 for k <= 4) into block positions
+    // flatten the runs (<= 27 for k <= 4) into blocks
     const int64_t rb = cell_runs[c], re = cell_runs[c + 1];
     const int nr = int(re - rb);
     uint2 myrun = make_uint2(0u, 0u);
@@ -154,9 +183,20 @@ __global__ void __launch_bounds__(128)
     for (int q0 = 0; q0 < nq; q0 += 32) {
       const int j = q0 + lane;  // query index within the cell
       const bool active = j < nq;
+      const int cnt = active ? int(qcount[cs + j]) : 0;
+      int ci = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) ci += t;
+      }
+      const int poff = ci - cnt;
+      const bool pooled = poff + cnt <= kExpandPool;  // otherwise straight to the final row
       const uint32_t qrow = active ? perm[cs + j] : 0u;
       uint32_t* dst = nbr + (active ? offsets[qrow] : 0);
-      const int g = j >> 3, col = j & 7;
+      const int gs = q0 >> 3;                    // first group of the slice
+      const int ngs = min(4, ngc - gs);          // groups in the slice
+      const int gl = lane >> 3, col = lane & 7;  // my group within the slice, my column
       const unsigned word = col & 1, sh = col >> 1;
       int o = 0;
       for (int b0 = 0; b0 < total; b0 += kExpandBlk) {
@@ -167,35 +207,61 @@ __global__ void __launch_bounds__(128)
           for (int b = lo; b < hi; ++b) bpos[b - b0] = myrun.x + 8u * uint32_t(b - myfirst);
         }
         __syncwarp();
+        // original ids of the blocks' candidates and the slice's masks (coalesced)
+        for (int i = lane; i < nb * 8; i += 32) {
+          const int b = i >> 3;
+          const uint32_t p = bpos[b] + uint32_t(i & 7);
+          bids[i] = p < n_points ? __ldg(perm + p) : 0u;  // rows past a run end: never hit
+        }
+        for (int i = lane; i < nb * 4; i += 32) {
+          const int b = i >> 2, g = i & 3;
+          bmsk[i] = g < ngs ? __ldg(mb + size_t(b0 + b) * ngc + gs + g) : 0ull;
+        }
+        __syncwarp();
         if (active) {
           for (int b = 0; b < nb; ++b) {
-            const unsigned long long m = mb[size_t(b0 + b) * ngc + g];
-            unsigned bits = (unsigned(m >> (32 * word)) >> sh) & 0x11111111u;
-            if (bits) {
-              const uint32_t p = bpos[b];
-              do {
-                const int r = (__ffs(bits) - 1) >> 2;
-                bits &= bits - 1;
-                dst[o++] = perm[p + r];
-              } while (bits);
+            unsigned bits =
+                (unsigned(bmsk[4 * b + gl] >> (32 * word)) >> sh) & 0x11111111u;
+            while (bits) {
+              const int r = (__ffs(bits) - 1) >> 2;
+              bits &= bits - 1;
+              const uint32_t v = bids[8 * b + r];
+              if (pooled) pool[poff + o] = v;
+              else dst[o] = v;
+              ++o;
             }
           }
         }
       }
       __syncwarp();
-      // sort the slice's rows (lane j's count is o)
+      // sort the slice's rows and store them
       const int nrows = min(32, nq - q0);
       for (int k = 0; k < nrows; ++k) {
-        const int len = __shfl_sync(0xffffffffu, o, k);
+        const int len = __shfl_sync(0xffffffffu, cnt, k);
+        const int off = __shfl_sync(0xffffffffu, poff, k);
+        const bool pk = __shfl_sync(0xffffffffu, pooled ? 1 : 0, k) != 0;
         const uint32_t rrow = __shfl_sync(0xffffffffu, qrow, k);
         uint32_t* row = nbr + offsets[rrow];
-        if (len <= 1) continue;
-        if (len <= 32) warp_sort_row<1>(row, len);
-        else if (len <= 64) warp_sort_row<2>(row, len);
-        else if (len <= 128) warp_sort_row<4>(row, len);
-        else if (len <= kWarpSortMax) warp_sort_row<8>(row, len);
-        else if (lane == 0) big_rows[atomicAdd(n_big, 1ull)] = rrow;
+        if (pk && len <= kWarpSortMax) {
+          if (len <= 32) sort_store_row<1>(pool + off, len, row);
+          else if (len <= 64) sort_store_row<2>(pool + off, len, row);
+          else if (len <= 128) sort_store_row<4>(pool + off, len, row);
+          else sort_store_row<8>(pool + off, len, row);
+        } else if (pk) {  // long pooled row: copy out, the CTA / radix path sorts it
+          for (int i = lane; i < len; i += 32) row[i] = pool[off + i];
+          if (lane == 0) big_rows[atomicAdd(n_big, 1ull)] = rrow;
+        } else if (len > 1) {  // written in place
+          if (len <= kWarpSortMax) {
+            if (len <= 32) warp_sort_row<1>(row, len);
+            else if (len <= 64) warp_sort_row<2>(row, len);
+            else if (len <= 128) warp_sort_row<4>(row, len);
+            else warp_sort_row<8>(row, len);
+          } else if (lane == 0) {
+            big_rows[atomicAdd(n_big, 1ull)] = rrow;
+          }
+        }
       }
+      __syncwarp();
     }
   }
 }
@@ -351,7 +417,8 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     expand_masks_kernel<<<unsigned(std::min<int64_t>(ceil_div(nc, 4), kNumSMs * 64)), 128, 0, s>>>(
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(), nc,
-        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), offsets, nbr, fill, nbig);
+        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), offsets, nbr, fill, nbig,
+        uint32_t(n));
     TJ_CHECK_LAUNCH();
   } else {
     TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));

@@ -76,6 +76,7 @@ struct RefineArgs {
   const double* P;         // (n, d_pad) cell-ordered coordinates
   const double* NRM;       // (n) squared norms (any rounding order; the guard covers it)
   const double* CN;        // (n, nchunks) chunk norms, reference order (kernels.py:126-130)
+  const double* SFX;       // (n, 4) chunk-norm suffixes after each short-circuit check point
   const uint2* runs;       // (n_runs) candidate position ranges [begin, end)
   const uint32_t* run_off; // (n_runs) offset of each run inside its cell's concatenation
   const int64_t* cell_runs;   // (n_cells+1)
@@ -118,7 +119,7 @@ struct tj_ctx {
   tj::GridState g;
   // grid buffers
   tj::DevBuf P, NRM, CN, perm, keys, cell_key, cell_start, cell_runs, runs, run_off, cell_cand,
-      cell_cost, dense;
+      cell_cost, dense, SFX;
   // scratch
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
   // results
@@ -146,11 +147,11 @@ ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
 int64_t build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
-void launch_refine_dmma(const RefineArgs& a, cudaStream_t s);
+void launch_refine_tc(const RefineArgs& a, cudaStream_t s);  // DMMA, 5 <= d <= 64
 void launch_refine_lowd(const RefineArgs& a, cudaStream_t s);  // d <= 4, unsliced items
 int lowd_queries_per_item();
 int core_queries_per_item(int d, int d_pad);
-int dmma_queries_per_item(int d, int d_pad);
+int tc_queries_per_item(int d_pad);
 // finalize.cu
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
                   int64_t n_mask_hits, cudaStream_t s);
