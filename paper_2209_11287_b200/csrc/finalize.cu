@@ -2,14 +2,17 @@
 //
 // Replaces the concatenate + np.lexsort((j, i)) of join.py:203-204.  Per-query
 // pair counts (cell-ordered positions) move to original-id order and are
-// scanned into int64 row offsets.  Then:
-//  * low-d path (row segments, refine_lowd.cu): one warp per query gathers its
-//    segment chain, maps candidate positions to original ids, sorts the row in
-//    registers (bitonic network) and writes it to its final place;
+// scanned into int64 row offsets; a second scan in position order gives every
+// row a contiguous slot range in a cell-ordered staging array.  Then:
+//  * low-d path (hit masks, refine_lowd.cu): warp per cell expands the masks of
+//    its query slices into the staging rows (expand_masks_kernel);
 //  * pair path (other kernels): every (query, candidate) pair is scattered to
-//    its row through a per-row atomic cursor, then each row is sorted in place.
-// Rows longer than 256 ids are sorted by one CTA (shared-memory bitonic, <= 8192)
-// or, beyond that, by a composite-key radix sort.
+//    its staging row through a per-row atomic cursor;
+//  * sort_rows_kernel reads 32 consecutive staging rows (coalesced), sorts one
+//    row per lane in registers (odd-even merge network) and writes each row to
+//    its final place.  Rows longer than 96 ids are sorted in place by a warp
+//    (<= 256), one CTA (shared-memory bitonic, <= 8192) or, beyond that, by a
+//    composite-key radix sort.
 #include "internal.cuh"
 #include "scan.cuh"
 
@@ -23,16 +26,17 @@ __global__ void counts_to_orig_kernel(const uint32_t* __restrict__ qcount,
     cnt_orig[perm[p]] = qcount[p];
 }
 
+// Pair path: (query position, candidate position) -> the query's row in cell
+// (position) order through a per-row atomic cursor; ids are original ids.
 __global__ void scatter_pairs_kernel(const uint2* __restrict__ pairs, int64_t total,
                                      const uint32_t* __restrict__ perm,
-                                     const int64_t* __restrict__ offsets,
-                                     uint32_t* __restrict__ fill, uint32_t* __restrict__ nbr) {
+                                     const int64_t* __restrict__ pos_off,
+                                     uint32_t* __restrict__ fill, uint32_t* __restrict__ rows) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const uint2 pr = pairs[e];
-    const uint32_t row = perm[pr.x];
-    const uint32_t slot = atomicAdd(&fill[row], 1u);
-    nbr[offsets[row] + slot] = perm[pr.y];
+    const uint32_t slot = atomicAdd(&fill[pr.x], 1u);
+    rows[pos_off[pr.x] + slot] = perm[pr.y];
   }
 }
 
@@ -94,52 +98,199 @@ __device__ __forceinline__ void warp_sort_row(uint32_t* row, int len) {
 constexpr int kWarpSortMax = 256;
 constexpr int kBlockSortMax = 8192;
 
-__global__ void sort_rows_warp_kernel(const int64_t* __restrict__ offsets, int64_t n,
-                                      uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
-                                      unsigned long long* n_big) {
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n; i += warps) {
-    const int64_t b = offsets[i];
-    const int64_t len = offsets[i + 1] - b;
-    if (len <= 1) continue;
-    uint32_t* row = nbr + b;
-    if (len <= 32) warp_sort_row<1>(row, int(len));
-    else if (len <= 64) warp_sort_row<2>(row, int(len));
-    else if (len <= 128) warp_sort_row<4>(row, int(len));
-    else if (len <= kWarpSortMax) warp_sort_row<8>(row, int(len));
-    else if (lane_id() == 0) big_rows[atomicAdd(n_big, 1ull)] = uint32_t(i);
+// ---------------------------------------------------------------- row batches
+// Short rows are sorted one per lane: a warp holds up to 32 rows in a
+// transposed shared-memory pool (slot i of column c at pool[i * kPoolLd + c];
+// the odd leading dimension keeps both the per-lane column walk and the
+// per-row copy-out conflict-free), each lane pulls its row into registers and
+// runs Batcher's odd-even merge sort on them.  The network is a compile-time
+// constant; slots past the row end hold 0xffffffff, so every comparator that
+// touches the padding folds away and a network of N slots costs only its
+// data-dependent min/max pairs (N = 64: 543 comparators, ~34 warp
+// instructions per row when the warp is full) -- versus ~300 for a warp-wide
+// bitonic sort of the same row.
+constexpr int kPoolSlots = 96;
+constexpr int kPoolLd = 33;
+
+// Comparator list of Batcher's odd-even merge sort for N keys (the network of
+// the next power of two restricted to the first N slots), built at compile time.
+template <int N>
+struct OemNet {
+  static constexpr int NP = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : 128;
+  template <typename F>
+  __host__ __device__ static constexpr void walk(F&& f) {
+    for (int p = 1; p < NP; p <<= 1)
+      for (int k = p; k >= 1; k >>= 1)
+        for (int j = k % p; j + k < NP; j += 2 * k)
+          for (int i = 0; i < k; ++i) {
+            const int x = i + j, y = i + j + k;
+            if (y < N && (x / (2 * p)) == (y / (2 * p))) f(x, y);
+          }
+  }
+  __host__ __device__ static constexpr int count() {
+    int c = 0;
+    walk([&](int, int) { ++c; });
+    return c;
+  }
+  static constexpr int C = count();
+  struct List {
+    unsigned char x[C], y[C];
+  };
+  __host__ __device__ static constexpr List list() {
+    List l{};
+    int c = 0;
+    walk([&](int x, int y) {
+      l.x[c] = (unsigned char)x;
+      l.y[c] = (unsigned char)y;
+      ++c;
+    });
+    return l;
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void oem_sort(uint32_t (&v)[N]) {
+  constexpr auto net = OemNet<N>::list();
+#pragma unroll
+  for (int t = 0; t < OemNet<N>::C; ++t) {
+    const uint32_t a = v[net.x[t]], b = v[net.y[t]];
+    v[net.x[t]] = min(a, b);
+    v[net.y[t]] = max(a, b);
   }
 }
 
-// Low-d hit masks -> rows.  Warp per cell: the cell's candidate runs are
-// re-flattened into 8-candidate blocks exactly as the refine kernel tiled them;
-// lane j owns query j of the current 32-query slice, walks the blocks, extracts
-// its column of each tile mask (bit 4r + (c>>1) of the low / high word for even /
-// odd column c) and writes the original ids of its hits to its final row; then
-// the warp sorts the slice's rows (bitonic in registers, long rows deferred).
-// Rows of the slice are built in a per-warp shared-memory pool and sorted from
-// there (one coalesced store per row); masks and the original ids of each
-// block's candidates are staged in shared memory first, so the per-hit work is
-// shared-memory only.
-constexpr int kExpandBlk = 64;  // blocks staged per chunk
-constexpr int kExpandPool = 1536;
-constexpr int kExpandWarps = 4;
+template <int N>
+__device__ __noinline__ void pool_sort_n(uint32_t* pool, int len) {
+  const int lane = lane_id();
+  uint32_t v[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = i < len ? pool[i * kPoolLd + lane] : 0xffffffffu;
+  oem_sort<N>(v);
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (i < len) pool[i * kPoolLd + lane] = v[i];
+}
 
-template <int R>
-__device__ __forceinline__ void sort_store_row(const uint32_t* src, int len, uint32_t* dst) {
-  uint32_t v[R];
+// Sort column `lane` of the pool (len <= kPoolSlots ids; 0 = no row).
+__device__ __noinline__ void pool_sort(uint32_t* pool, int len) {
+  int mx = len;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = r * 32 + lane_id();
-    v[r] = i < len ? src[i] : 0xffffffffu;
-  }
-  warp_bitonic<R>(v);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (mx <= 1) return;
+  if (mx <= 16) pool_sort_n<16>(pool, len);
+  else if (mx <= 32) pool_sort_n<32>(pool, len);
+  else if (mx <= 48) pool_sort_n<48>(pool, len);
+  else if (mx <= 64) pool_sort_n<64>(pool, len);
+  else if (mx <= 80) pool_sort_n<80>(pool, len);
+  else pool_sort_n<96>(pool, len);
+}
+
+// Rows with more than kPoolSlots ids are written straight to their place and
+// sorted there: by the warp (<= kWarpSortMax) or listed for the CTA/radix path.
+__device__ __noinline__ void sort_long_row(uint32_t* row, int len, uint32_t id, uint32_t* big_rows,
+                                           unsigned long long* n_big) {
+  if (len <= 128) warp_sort_row<4>(row, len);
+  else if (len <= kWarpSortMax) warp_sort_row<8>(row, len);
+  else if (lane_id() == 0) big_rows[atomicAdd(n_big, 1ull)] = id;
+}
+
+// Rows in cell order -> final CSR.  Warp per 32 consecutive query positions:
+// their rows are one contiguous segment of `rows` (position-order offsets
+// pos_off), read row by row with 16 rows' loads in flight before their
+// shared-memory stores into the rows' pool columns.  Each lane then sorts one
+// row in registers (odd-even merge network) and the warp writes the sorted rows
+// to their places.  Rows longer than kPoolSlots are copied to their place and
+// sorted there (warp bitonic <= kWarpSortMax, else listed for the CTA / radix
+// path).
+constexpr int kSortWarps = 4;
+constexpr int kSortGroup = 16;  // rows loaded per group
+
+__global__ void __launch_bounds__(kSortWarps * 32)
+    sort_rows_kernel(const int64_t* __restrict__ pos_off, const uint32_t* __restrict__ rows,
+                     const uint32_t* __restrict__ perm, const int64_t* __restrict__ offsets,
+                     int64_t n, uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
+                     unsigned long long* n_big) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  uint32_t* pool = reinterpret_cast<uint32_t*>(smem_raw) + warp * kPoolSlots * kPoolLd;
+  const int64_t warps = int64_t(gridDim.x) * kSortWarps;
+  for (int64_t p0 = (int64_t(blockIdx.x) * kSortWarps + warp) * 32; p0 < n; p0 += warps * 32) {
+    const int64_t p = p0 + lane;
+    const int64_t src = p < n ? pos_off[p] : 0;
+    const int len = p < n ? int(pos_off[p + 1] - src) : 0;
+    const uint32_t id = p < n ? perm[p] : 0u;
+    const int64_t dst = p < n ? offsets[id] : 0;
+    const int nrows = int(min(int64_t(32), n - p0));
+    __syncwarp();
+    for (int k0 = 0; k0 < nrows; k0 += kSortGroup) {
+      uint32_t v[kSortGroup][3];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = r * 32 + lane_id();
-    if (i < len) dst[i] = v[r];
+      for (int kk = 0; kk < kSortGroup; ++kk) {
+        const int L = __shfl_sync(0xffffffffu, len, (k0 + kk) & 31);
+        const int64_t S = __shfl_sync(0xffffffffu, src, (k0 + kk) & 31);
+        const bool ok = k0 + kk < nrows && L <= kPoolSlots;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int e = lane + 32 * t;
+          v[kk][t] = (ok && e < L) ? __ldg(rows + S + e) : 0u;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < kSortGroup; ++kk) {
+        const int L = __shfl_sync(0xffffffffu, len, (k0 + kk) & 31);
+        const bool ok = k0 + kk < nrows && L <= kPoolSlots;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int e = lane + 32 * t;
+          if (ok && e < L) pool[e * kPoolLd + k0 + kk] = v[kk][t];
+        }
+      }
+    }
+    __syncwarp();
+    pool_sort(pool, len <= kPoolSlots ? len : 0);
+    __syncwarp();
+    for (int k = 0; k < nrows; ++k) {
+      const int L = __shfl_sync(0xffffffffu, len, k);
+      const int64_t D = __shfl_sync(0xffffffffu, dst, k);
+      if (L <= kPoolSlots) {
+        for (int e = lane; e < L; e += 32) nbr[D + e] = pool[e * kPoolLd + k];
+      } else {
+        const int64_t S = __shfl_sync(0xffffffffu, src, k);
+        for (int e = lane; e < L; e += 32) nbr[D + e] = rows[S + e];
+        __syncwarp();
+        sort_long_row(nbr + D, L, __shfl_sync(0xffffffffu, id, k), big_rows, n_big);
+      }
+    }
   }
 }
+
+// Low-d hit masks -> rows in cell order (unsorted; sort_rows_kernel orders).  Warp
+// per cell: the cell's candidate runs are re-flattened into 8-candidate blocks
+// exactly as the refine kernel tiled them.  For each chunk of blocks the
+// original ids of the blocks' candidates and the current query slice's masks
+// (<= 4 groups of 8 queries) are staged with wide independent loads; the masks
+// are split into 32-bit halves and compacted to the non-empty ones.  Lanes then
+// drain one hit per iteration and grab the next half from a shared counter
+// (hits cluster in the blocks nearest the query cell, so any static split
+// leaves most lanes idle); bit 4r + c of a low / high half is candidate r of the
+// block against query column 2c / 2c + 1.  A per-query shared-memory cursor
+// hands out slots in a flat slice buffer (row order is irrelevant before the
+// sort), and the slice's rows are copied out with coalesced stores.  Rows that
+// do not fit the buffer are written straight to their place.
+constexpr int kExpandBlk = 64;     // blocks staged per chunk
+constexpr int kExpandWarps = 8;
+constexpr int kSliceBuf = 1536;    // ids buffered per query slice
+
+struct ExpandSmem {
+  uint32_t buf[kSliceBuf];
+  uint32_t pos[kExpandBlk];
+  uint32_t ids[kExpandBlk * 8];
+  uint2 units[kExpandBlk * 8];  // non-empty mask halves: (bits, ids index << 8 | column)
+  int64_t dst[32];              // row start per query of the slice
+  uint32_t slot[32];            // next free slot per query (buffer index or row index)
+  uint32_t next;                // dynamic unit counter
+  uint32_t direct;              // bit j: query j writes straight to its row
+};
 
 __global__ void __launch_bounds__(kExpandWarps * 32)
     expand_masks_kernel(const unsigned long long* __restrict__ masks,
@@ -147,23 +298,18 @@ __global__ void __launch_bounds__(kExpandWarps * 32)
                         const int64_t* __restrict__ cell_start,
                         const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
                         int64_t n_cells, const uint32_t* __restrict__ qcount,
-                        const uint32_t* __restrict__ perm, const int64_t* __restrict__ offsets,
-                        uint32_t* __restrict__ nbr, uint32_t* __restrict__ big_rows,
-                        unsigned long long* n_big, uint32_t n_points) {
-  __shared__ uint32_t s_pos[kExpandWarps][kExpandBlk];
-  __shared__ uint32_t s_ids[kExpandWarps][kExpandBlk * 8];
-  __shared__ unsigned long long s_msk[kExpandWarps][kExpandBlk * 4];
-  __shared__ uint32_t s_pool[kExpandWarps][kExpandPool];
+                        const uint32_t* __restrict__ perm, const int64_t* __restrict__ pos_off,
+                        uint32_t* __restrict__ rows_out, uint32_t n_points) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  uint32_t* bpos = s_pos[warp];
-  uint32_t* bids = s_ids[warp];
-  unsigned long long* bmsk = s_msk[warp];
-  uint32_t* pool = s_pool[warp];
+  ExpandSmem& sm = reinterpret_cast<ExpandSmem*>(smem_raw)[warp];
+  const unsigned lt = lanemask_lt();
+
   const int64_t stride = int64_t(gridDim.x) * kExpandWarps;
   for (int64_t c = int64_t(blockIdx.x) * kExpandWarps + warp; c < n_cells; c += stride) {
     const int64_t cs = cell_start[c];
     const int nq = int(cell_start[c + 1] - cs);
-    if (qcount[cs] == 0) continue;  // cell not refined in this result set
+    if (qcount[cs] == 0) continue;  // cell not refined in this result set (self pair missing)
     const int ngc = (nq + 7) >> 3;
     // flatten the runs (<= 27 for k <= 4) into blocks
     const int64_t rb = cell_runs[c], re = cell_runs[c + 1];
@@ -181,9 +327,12 @@ __global__ void __launch_bounds__(kExpandWarps * 32)
     const int myfirst = incl - mynblk;
     const unsigned long long* mb = masks + cell_mbase[c];
     for (int q0 = 0; q0 < nq; q0 += 32) {
-      const int j = q0 + lane;  // query index within the cell
-      const bool active = j < nq;
-      const int cnt = active ? int(qcount[cs + j]) : 0;
+      const int nqs = min(32, nq - q0);
+      const int ngs = (nqs + 7) >> 3;
+      const int gs = q0 >> 3;  // first group of the slice
+      // query j of the slice (lane j): length, buffer offset, row start
+      const bool qa = lane < nqs;
+      const int cnt = qa ? int(qcount[cs + q0 + lane]) : 0;
       int ci = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -191,77 +340,93 @@ __global__ void __launch_bounds__(kExpandWarps * 32)
         if (lane >= o) ci += t;
       }
       const int poff = ci - cnt;
-      const bool pooled = poff + cnt <= kExpandPool;  // otherwise straight to the final row
-      const uint32_t qrow = active ? perm[cs + j] : 0u;
-      uint32_t* dst = nbr + (active ? offsets[qrow] : 0);
-      const int gs = q0 >> 3;                    // first group of the slice
-      const int ngs = min(4, ngc - gs);          // groups in the slice
-      const int gl = lane >> 3, col = lane & 7;  // my group within the slice, my column
-      const unsigned word = col & 1, sh = col >> 1;
-      int o = 0;
+      const bool pooled = poff + cnt <= kSliceBuf;
+      const int64_t dst = qa ? pos_off[cs + q0 + lane] : 0;  // row start, position order
+      __syncwarp();
+      if (qa) {
+        sm.dst[lane] = dst;
+        sm.slot[lane] = pooled ? uint32_t(poff) : 0u;
+      }
+      {
+        const unsigned dm = __ballot_sync(0xffffffffu, qa && !pooled);
+        if (lane == 0) sm.direct = dm;
+      }
       for (int b0 = 0; b0 < total; b0 += kExpandBlk) {
         const int nb = min(kExpandBlk, total - b0);
         __syncwarp();
         {
           const int lo = max(myfirst, b0), hi = min(myfirst + mynblk, b0 + nb);
-          for (int b = lo; b < hi; ++b) bpos[b - b0] = myrun.x + 8u * uint32_t(b - myfirst);
+          for (int b = lo; b < hi; ++b) sm.pos[b - b0] = myrun.x + 8u * uint32_t(b - myfirst);
         }
         __syncwarp();
-        // original ids of the blocks' candidates and the slice's masks (coalesced)
-        for (int i = lane; i < nb * 8; i += 32) {
-          const int b = i >> 3;
-          const uint32_t p = bpos[b] + uint32_t(i & 7);
-          bids[i] = p < n_points ? __ldg(perm + p) : 0u;  // rows past a run end: never hit
+        // original ids of the chunk's candidates: 4 loads in flight per lane
+        for (int i0 = 0; i0 < nb * 8; i0 += 128) {
+          uint32_t v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = i0 + 32 * k + lane;
+            const uint32_t p = i < nb * 8 ? sm.pos[i >> 3] + uint32_t(i & 7) : n_points;
+            v[k] = p < n_points ? __ldg(perm + p) : 0u;  // rows past a run end never hit
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = i0 + 32 * k + lane;
+            if (i < nb * 8) sm.ids[i] = v[k];
+          }
         }
-        for (int i = lane; i < nb * 4; i += 32) {
-          const int b = i >> 2, g = i & 3;
-          bmsk[i] = g < ngs ? __ldg(mb + size_t(b0 + b) * ngc + gs + g) : 0ull;
+        // the slice's mask words, split into halves and compacted to the non-empty ones
+        const int nw = nb * ngs;  // word w = (block w / ngs, group w % ngs)
+        int nunits = 0;
+        for (int i0 = 0; i0 < nw; i0 += 128) {
+          unsigned long long v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int w = i0 + 32 * k + lane;
+            const int b = ngs == 3 ? int((unsigned(w) * 0xAAABu) >> 17) : (w >> (ngs >> 1));
+            v[k] = w < nw ? __ldg(mb + size_t(b0 + b) * ngc + gs + (w - b * ngs)) : 0ull;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int w = i0 + 32 * k + lane;
+            const int b = ngs == 3 ? int((unsigned(w) * 0xAAABu) >> 17) : (w >> (ngs >> 1));
+            const unsigned meta = (unsigned(8 * b) << 8) | unsigned(8 * (w - b * ngs));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const unsigned bits = unsigned(v[k] >> (32 * h));
+              const unsigned bal = __ballot_sync(0xffffffffu, bits != 0u);
+              if (bits) sm.units[nunits + __popc(bal & lt)] = make_uint2(bits, meta + h);
+              nunits += __popc(bal);
+            }
+          }
         }
+        if (lane == 0) sm.next = 32;
         __syncwarp();
-        if (active) {
-          for (int b = 0; b < nb; ++b) {
-            unsigned bits =
-                (unsigned(bmsk[4 * b + gl] >> (32 * word)) >> sh) & 0x11111111u;
-            while (bits) {
-              const int r = (__ffs(bits) - 1) >> 2;
-              bits &= bits - 1;
-              const uint32_t v = bids[8 * b + r];
-              if (pooled) pool[poff + o] = v;
-              else dst[o] = v;
-              ++o;
+        const unsigned direct = sm.direct;
+        int k = lane;
+        uint2 e = k < nunits ? sm.units[k] : make_uint2(0u, 0u);
+        while (__any_sync(0xffffffffu, k < nunits)) {
+          if (k < nunits) {
+            const int j = __ffs(e.x) - 1;
+            e.x &= e.x - 1u;
+            const int col = int(e.y & 0xffu) + 2 * (j & 3);
+            const uint32_t v = sm.ids[(e.y >> 8) + (j >> 2)];
+            const uint32_t slot = atomicAdd(&sm.slot[col], 1u);
+            if (!((direct >> col) & 1u)) sm.buf[slot] = v;
+            else rows_out[sm.dst[col] + slot] = v;
+            if (e.x == 0u) {
+              k = int(atomicAdd(&sm.next, 1u));
+              if (k < nunits) e = sm.units[k];
             }
           }
         }
       }
       __syncwarp();
-      // sort the slice's rows and store them
-      const int nrows = min(32, nq - q0);
-      for (int k = 0; k < nrows; ++k) {
-        const int len = __shfl_sync(0xffffffffu, cnt, k);
-        const int off = __shfl_sync(0xffffffffu, poff, k);
-        const bool pk = __shfl_sync(0xffffffffu, pooled ? 1 : 0, k) != 0;
-        const uint32_t rrow = __shfl_sync(0xffffffffu, qrow, k);
-        uint32_t* row = nbr + offsets[rrow];
-        if (pk && len <= kWarpSortMax) {
-          if (len <= 32) sort_store_row<1>(pool + off, len, row);
-          else if (len <= 64) sort_store_row<2>(pool + off, len, row);
-          else if (len <= 128) sort_store_row<4>(pool + off, len, row);
-          else sort_store_row<8>(pool + off, len, row);
-        } else if (pk) {  // long pooled row: copy out, the CTA / radix path sorts it
-          for (int i = lane; i < len; i += 32) row[i] = pool[off + i];
-          if (lane == 0) big_rows[atomicAdd(n_big, 1ull)] = rrow;
-        } else if (len > 1) {  // written in place
-          if (len <= kWarpSortMax) {
-            if (len <= 32) warp_sort_row<1>(row, len);
-            else if (len <= 64) warp_sort_row<2>(row, len);
-            else if (len <= 128) warp_sort_row<4>(row, len);
-            else warp_sort_row<8>(row, len);
-          } else if (lane == 0) {
-            big_rows[atomicAdd(n_big, 1ull)] = rrow;
-          }
-        }
-      }
-      __syncwarp();
+      // the buffered rows (a prefix of the slice) are contiguous in rows_out too
+      int pend = (qa && pooled) ? poff + cnt : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pend = max(pend, __shfl_xor_sync(0xffffffffu, pend, o));
+      const int64_t d0 = __shfl_sync(0xffffffffu, dst, 0);
+      for (int i = lane; i < pend; i += 32) rows_out[d0 + i] = sm.buf[i];
     }
   }
 }
@@ -408,25 +573,51 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
   TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   if (n_pairs == 0 && n_mask_hits == 0) return;
 
+  // rows in cell (position) order first: offsets by position, then the ids
+  ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
+  int64_t* pos_off = ctx->pos_off.as<int64_t>();
+  scan_exclusive(LoadAt<uint32_t>{ctx->qcount.as<uint32_t>()}, StoreAt<int64_t>{pos_off}, n, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(pos_off + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  const int64_t total = n_pairs + n_mask_hits;
+  ctx->rows_tmp.ensure(sizeof(uint32_t) * std::max<int64_t>(total, 1), s);
+  uint32_t* rows = ctx->rows_tmp.as<uint32_t>();
   ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
   uint32_t* fill = ctx->fill.as<uint32_t>();
   unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
   TJ_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
   if (n_mask_hits > 0) {
     const int64_t nc = ctx->g.n_cells;
-    expand_masks_kernel<<<unsigned(std::min<int64_t>(ceil_div(nc, 4), kNumSMs * 64)), 128, 0, s>>>(
+    const size_t smem = sizeof(ExpandSmem) * kExpandWarps;
+    TJ_CUDA(cudaFuncSetAttribute(expand_masks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    int per_sm = 0;
+    TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_masks_kernel,
+                                                          kExpandWarps * 32, smem));
+    const int64_t grid = std::min<int64_t>(ceil_div(nc, kExpandWarps),
+                                           int64_t(kNumSMs) * std::max(per_sm, 1));
+    expand_masks_kernel<<<unsigned(std::max<int64_t>(grid, 1)), kExpandWarps * 32, smem, s>>>(
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(), nc,
-        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), offsets, nbr, fill, nbig,
-        uint32_t(n));
+        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), pos_off, rows, uint32_t(n));
     TJ_CHECK_LAUNCH();
   } else {
     TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
     scatter_pairs_kernel<<<blocks_for(n_pairs, 256), 256, 0, s>>>(
-        ctx->pairs.as<uint2>(), n_pairs, ctx->perm.as<uint32_t>(), offsets, fill, nbr);
+        ctx->pairs.as<uint2>(), n_pairs, ctx->perm.as<uint32_t>(), pos_off, fill, rows);
     TJ_CHECK_LAUNCH();
-    // `fill` becomes the list of long rows once the scatter is done (same stream)
-    sort_rows_warp_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(offsets, n, nbr, fill, nbig);
+  }
+  // sort each row into its final place; `fill` becomes the list of long rows
+  {
+    const size_t smem = sizeof(uint32_t) * kPoolSlots * kPoolLd * kSortWarps;
+    TJ_CUDA(cudaFuncSetAttribute(sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    int per_sm = 0;
+    TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_rows_kernel,
+                                                          kSortWarps * 32, smem));
+    const int64_t grid = std::min<int64_t>(ceil_div(n, 32 * kSortWarps),
+                                           int64_t(kNumSMs) * std::max(per_sm, 1));
+    sort_rows_kernel<<<unsigned(std::max<int64_t>(grid, 1)), kSortWarps * 32, smem, s>>>(
+        pos_off, rows, ctx->perm.as<uint32_t>(), offsets, n, nbr, fill, nbig);
     TJ_CHECK_LAUNCH();
   }
   sort_big_rows(ctx, offsets, nbr, fill, nbig, s);

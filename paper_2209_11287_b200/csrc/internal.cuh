@@ -124,6 +124,7 @@ struct tj_ctx {
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
   // results
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_blocks, cell_mbase;
+  tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
   unsigned long long pair_cap = 0;
   int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
   int64_t n_items = 0;
