@@ -167,6 +167,13 @@ def barrier(world: int):
         dist.barrier()
 
 
+def refine_kernel_name(kernel: str, d: int) -> str:
+    """The refine kernel tj_refine dispatches to (capi.cu)."""
+    if kernel == "scalar":
+        return "refine_core_kernel"
+    return "refine_lowd_kernel" if d <= 4 else "refine_tc_kernel"
+
+
 def traffic_from_profiles(config: str, kernel: str):
     """DRAM bytes per refine launch from the committed ncu --set full summary, if any."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -423,7 +430,7 @@ def run_ours(args, world, rank, local):
                                            "finalize_ms")},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic_from_profiles(args.config, args.kernel),
-                     "kernel": "refine_dmma_kernel" if args.kernel == "tile" else "refine_core_kernel",
+                     "kernel": refine_kernel_name(args.kernel, d),
                      "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, DFMA {peak_dfma:.2f}) TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
                      "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))",
                      "share_of_step": share},
