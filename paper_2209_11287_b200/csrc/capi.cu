@@ -61,6 +61,7 @@ static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
   if (ctx->masks_ready) return;
   const int64_t total = build_mask_bases(ctx, 0, ctx->g.n_cells, s);
   ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(total, 1), s);
+  build_window_cells(ctx, s);
   ctx->masks_ready = true;
 }
 
@@ -123,7 +124,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->cell_cand, &ctx->cell_cost, &ctx->keys_alt,  &ctx->vals_alt,  &ctx->sort_hist,
                     &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
                     &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
-                    &ctx->masks,    &ctx->cell_blocks, &ctx->cell_mbase, &ctx->dense};
+                    &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
+                    &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -269,7 +271,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
       reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
     }
     if (lowd) ensure_masks(ctx, s);
-    const int qpi = lowd ? lowd_queries_per_item()
+    const int qpi = lowd ? lowd_queries_per_item(g.n, g.n_cells)
                     : dmma ? tc_queries_per_item(g.d_pad)
                            : core_queries_per_item(g.d, g.d_pad);
     // lowd: items never split a candidate list (each query row comes from one item)
@@ -294,7 +296,6 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.qcount = ctx->qcount.as<uint32_t>();
     a.masks = ctx->masks.as<unsigned long long>();
     a.cell_mbase = ctx->cell_mbase.as<int64_t>();
-    a.cell_blocks = ctx->cell_blocks.as<int64_t>();
     a.cell_base = 0;
     a.d = g.d;
     a.d_pad = g.d_pad;
@@ -304,11 +305,13 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.max_norm = g.max_norm + g.eps_sq;
     a.short_circuit = short_circuit ? 1 : 0;
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
-    if (lowd) launch_refine_lowd(a, s);
+    if (lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
     else if (dmma) launch_refine_tc(a, s);
     else launch_refine_core(a, s);
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;
+    // low-d rows are counted from the hit masks (pairs per query + total hits)
+    if (lowd) launch_count_rows(ctx, cell_begin, cell_end, &counters(ctx)->hits, s);
   });
 }
 

@@ -4,15 +4,17 @@
 // pair counts (cell-ordered positions) move to original-id order and are
 // scanned into int64 row offsets; a second scan in position order gives every
 // row a contiguous slot range in a cell-ordered staging array.  Then:
-//  * low-d path (hit masks, refine_lowd.cu): warp per cell expands the masks of
-//    its query slices into the staging rows (expand_masks_kernel);
+//  * low-d path (hit masks, refine_lowd.cu): emit_rows_kernel expands the masks
+//    of 32 consecutive query positions straight into a shared-memory pool,
+//    sorts one row per lane in registers and writes the rows to their places;
 //  * pair path (other kernels): every (query, candidate) pair is scattered to
-//    its staging row through a per-row atomic cursor;
-//  * sort_rows_kernel reads 32 consecutive staging rows (coalesced), sorts one
-//    row per lane in registers (odd-even merge network) and writes each row to
-//    its final place.  Rows longer than 96 ids are sorted in place by a warp
-//    (<= 256), one CTA (shared-memory bitonic, <= 8192) or, beyond that, by a
-//    composite-key radix sort.
+//    a staging row in cell order through a per-row atomic cursor (a second
+//    scan in position order places the rows), then sort_rows_kernel reads 32
+//    consecutive staging rows (coalesced), sorts one row per lane and writes
+//    each row to its final place.
+//  Rows longer than 96 ids are sorted in place by a warp (<= 256), one CTA
+//  (shared-memory bitonic, <= 8192) or, beyond that, by a composite-key radix
+//  sort.
 #include "internal.cuh"
 #include "scan.cuh"
 
@@ -264,170 +266,293 @@ __global__ void __launch_bounds__(kSortWarps * 32)
   }
 }
 
-// Low-d hit masks -> rows in cell order (unsorted; sort_rows_kernel orders).  Warp
-// per cell: the cell's candidate runs are re-flattened into 8-candidate blocks
-// exactly as the refine kernel tiled them.  For each chunk of blocks the
-// original ids of the blocks' candidates and the current query slice's masks
-// (<= 4 groups of 8 queries) are staged with wide independent loads; the masks
-// are split into 32-bit halves and compacted to the non-empty ones.  Lanes then
-// drain one hit per iteration and grab the next half from a shared counter
-// (hits cluster in the blocks nearest the query cell, so any static split
-// leaves most lanes idle); bit 4r + c of a low / high half is candidate r of the
-// block against query column 2c / 2c + 1.  A per-query shared-memory cursor
-// hands out slots in a flat slice buffer (row order is irrelevant before the
-// sort), and the slice's rows are copied out with coalesced stores.  Rows that
-// do not fit the buffer are written straight to their place.
-constexpr int kExpandBlk = 64;     // blocks staged per chunk
-constexpr int kExpandWarps = 8;
-constexpr int kSliceBuf = 1536;    // ids buffered per query slice
+// ------------------------------------------------------------ low-d masks
+// Rows of the low-d path are read straight out of the refine kernel's hit
+// masks.  Query position p of cell c sits in group g = (p - cs) / 8 of its
+// cell, column (p - cs) % 8; its hits against block b are the bits
+// 4r + col/2 (+32 for odd columns) of mask (g, b), i.e. candidate 8b + r of
+// the cell's concatenated list.  Every kernel below walks windows of 32
+// consecutive positions, lane j = position 32w + j.
 
-struct ExpandSmem {
-  uint32_t buf[kSliceBuf];
-  uint32_t pos[kExpandBlk];
-  uint32_t ids[kExpandBlk * 8];
-  uint2 units[kExpandBlk * 8];  // non-empty mask halves: (bits, ids index << 8 | column)
-  int64_t dst[32];              // row start per query of the slice
-  uint32_t slot[32];            // next free slot per query (buffer index or row index)
-  uint32_t next;                // dynamic unit counter
-  uint32_t direct;              // bit j: query j writes straight to its row
+// Cell of this lane's position: c0 = cell containing the window start; the
+// cells starting inside the window are found with one load per lane.
+__device__ __forceinline__ int64_t window_lane_cell(const int64_t* __restrict__ cell_start,
+                                                    int64_t n_cells, int64_t c0, int64_t p0) {
+  const int lane = lane_id();
+  const int64_t cl = c0 + lane;
+  const int64_t cs_l = cl <= n_cells ? cell_start[cl] : INT64_MAX;
+  const int64_t off = cs_l - p0;
+  const unsigned bit = (off >= 0 && off < 32) ? (1u << unsigned(off)) : 0u;
+  const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
+  const unsigned upto = (2u << lane) - 1u;  // lanes <= this one (wraps to all at lane 31)
+  return c0 + __popc(starts & upto) - int(starts & 1u);
+}
+
+struct MaskRow {
+  const unsigned long long* m;  // the row's group: nblk masks
+  int nblk;
+  int shift;                    // 32 * (col & 1) + col / 2
 };
 
-__global__ void __launch_bounds__(kExpandWarps * 32)
-    expand_masks_kernel(const unsigned long long* __restrict__ masks,
-                        const int64_t* __restrict__ cell_mbase,
-                        const int64_t* __restrict__ cell_start,
-                        const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
-                        int64_t n_cells, const uint32_t* __restrict__ qcount,
-                        const uint32_t* __restrict__ perm, const int64_t* __restrict__ pos_off,
-                        uint32_t* __restrict__ rows_out, uint32_t n_points) {
+__device__ __forceinline__ MaskRow mask_row(const unsigned long long* __restrict__ masks,
+                                            const int64_t* __restrict__ cell_mbase,
+                                            const int64_t* __restrict__ cell_cand, int64_t c,
+                                            int64_t rel) {
+  MaskRow r;
+  r.nblk = int((cell_cand[c] + 7) >> 3);
+  r.m = masks + cell_mbase[c] + (rel >> 3) * r.nblk;
+  const int col = int(rel & 7);
+  r.shift = 32 * (col & 1) + (col >> 1);
+  return r;
+}
+
+__device__ __forceinline__ unsigned row_bits(unsigned long long m, int shift) {
+  return unsigned(m >> shift) & 0x11111111u;  // bit 4r: candidate r of the block
+}
+
+// Pairs per query of the cells [cb, ce) (their masks were just written).
+__global__ void __launch_bounds__(256)
+    count_rows_kernel(const unsigned long long* __restrict__ masks,
+                      const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
+                      const int64_t* __restrict__ cell_cand, int64_t n_cells,
+                      const uint32_t* __restrict__ win_cell, int64_t cb, int64_t ce,
+                      uint32_t* __restrict__ qcount, unsigned long long* hits) {
+  const int lane = lane_id();
+  const int64_t pb = cell_start[cb], pe = cell_start[ce];
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  unsigned long long tot = 0;
+  for (int64_t w = (pb >> 5) + (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
+       (w << 5) < pe; w += warps) {
+    const int64_t p0 = w << 5, p = p0 + lane;
+    const int64_t c = window_lane_cell(cell_start, n_cells, win_cell[w], p0);
+    if (p < pb || p >= pe) continue;
+    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
+    unsigned cnt = 0;
+    int b = 0;
+    for (; b + 4 <= mr.nblk; b += 4) {
+      unsigned long long v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(mr.m + b + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cnt += __popc(row_bits(v[u], mr.shift));
+    }
+    for (; b < mr.nblk; ++b) cnt += __popc(row_bits(__ldg(mr.m + b), mr.shift));
+    qcount[p] = cnt;
+    tot += cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0 && tot) atomicAdd(hits, tot);
+}
+
+// Candidate list offset t of a cell -> cell-ordered position (runs [rb, rb+nr)).
+__device__ __forceinline__ uint32_t run_position(const uint2* __restrict__ runs,
+                                                 const uint32_t* __restrict__ run_off, int64_t rb,
+                                                 int nr, uint32_t t) {
+  int lo = 0, hi = nr;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (run_off[rb + mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return runs[rb + lo].x + (t - run_off[rb + lo]);
+}
+
+// Short rows (<= kPoolSlots ids), one per lane, expanded, sorted and placed in
+// one pass.  The lane's mask row (its query group, ~1 KB) is first prefetched
+// into L1 with independent prefetches (one round trip instead of one per 4
+// masks); the lane then walks it and collects its candidate offsets in column
+// `lane` of a transposed shared-memory pool (ascending), maps them to positions
+// by a branch-free binary search in its cell's run table (shared memory,
+// staged once per window for up to kEmitCells cells) and to original ids with
+// 16 independent gathers in flight; the warp sorts the 32 rows in registers
+// (odd-even merge network) and writes them to their places.  Longer rows are
+// listed for long_rows_kernel (warp per row).
+constexpr int kEmitWarps = 4;
+constexpr int kEmitCells = 8;   // cells of one window whose run tables are staged
+constexpr int kRunTab = 32;     // >= 27 runs (k <= 4) + the list-length sentinel
+
+struct EmitSmem {
+  uint32_t pool[kPoolSlots * kPoolLd];
+  uint32_t roff[kEmitCells][kRunTab];  // run offsets, padded with 0xffffffff
+  uint32_t rpos[kEmitCells][kRunTab];  // run start positions
+};
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__global__ void __launch_bounds__(kEmitWarps * 32)
+    emit_rows_kernel(const unsigned long long* __restrict__ masks,
+                     const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
+                     const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
+                     const uint32_t* __restrict__ run_off, const int64_t* __restrict__ cell_cand,
+                     int64_t n_cells, const uint32_t* __restrict__ win_cell,
+                     const uint32_t* __restrict__ qcount, const uint32_t* __restrict__ perm,
+                     const int64_t* __restrict__ offsets, int64_t n, uint32_t* __restrict__ nbr,
+                     uint32_t* __restrict__ long_rows, unsigned long long* n_long) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  ExpandSmem& sm = reinterpret_cast<ExpandSmem*>(smem_raw)[warp];
-  const unsigned lt = lanemask_lt();
-
-  const int64_t stride = int64_t(gridDim.x) * kExpandWarps;
-  for (int64_t c = int64_t(blockIdx.x) * kExpandWarps + warp; c < n_cells; c += stride) {
-    const int64_t cs = cell_start[c];
-    const int nq = int(cell_start[c + 1] - cs);
-    if (qcount[cs] == 0) continue;  // cell not refined in this result set (self pair missing)
-    const int ngc = (nq + 7) >> 3;
-    // flatten the runs (<= 27 for k <= 4) into blocks
-    const int64_t rb = cell_runs[c], re = cell_runs[c + 1];
-    const int nr = int(re - rb);
-    uint2 myrun = make_uint2(0u, 0u);
-    if (lane < nr) myrun = runs[rb + lane];
-    const int mynblk = int(myrun.y - myrun.x + 7) >> 3;
-    int incl = mynblk;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+  EmitSmem& sm = reinterpret_cast<EmitSmem*>(smem_raw)[warp];
+  uint32_t* pool = sm.pool;
+  const int64_t n_win = (n + 31) >> 5;
+  const int64_t stride = int64_t(gridDim.x) * kEmitWarps;
+  for (int64_t w = int64_t(blockIdx.x) * kEmitWarps + warp; w < n_win; w += stride) {
+    const int64_t p0 = w << 5, p = p0 + lane;
+    const bool valid = p < n;
+    const int len = valid ? int(qcount[p]) : 0;
+    const uint32_t id = valid ? perm[p] : 0u;
+    const int64_t dst = valid ? offsets[id] : 0;
+    const int64_t c0 = win_cell[w];
+    const int64_t c = window_lane_cell(cell_start, n_cells, c0, p0);
+    const bool pooled = len > 0 && len <= kPoolSlots;
+    if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = uint32_t(p);
+    MaskRow mr{};
+    if (pooled) {
+      mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
+      for (int b = 0; b < mr.nblk; b += 4) prefetch_l1(mr.m + b);
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int myfirst = incl - mynblk;
-    const unsigned long long* mb = masks + cell_mbase[c];
-    for (int q0 = 0; q0 < nq; q0 += 32) {
-      const int nqs = min(32, nq - q0);
-      const int ngs = (nqs + 7) >> 3;
-      const int gs = q0 >> 3;  // first group of the slice
-      // query j of the slice (lane j): length, buffer offset, row start
-      const bool qa = lane < nqs;
-      const int cnt = qa ? int(qcount[cs + q0 + lane]) : 0;
-      int ci = cnt;
+    // run tables of the window's first kEmitCells cells (lanes = runs)
+    const int ncw = int(min(__shfl_sync(0xffffffffu, c, 31) + 1, n_cells) - c0);
+    __syncwarp();
+    for (int ci = 0; ci < min(ncw, kEmitCells); ++ci) {
+      const int64_t rb = cell_runs[c0 + ci], nr = cell_runs[c0 + ci + 1] - rb;
+      sm.roff[ci][lane] = lane < nr ? run_off[rb + lane] : 0xffffffffu;
+      sm.rpos[ci][lane] = lane < nr ? runs[rb + lane].x : 0u;
+    }
+    __syncwarp();
+    if (pooled) {
+      // 1. candidate offsets, ascending
+      uint32_t* col = pool + lane;
+      int slot = 0;
+      for (int b0 = 0; b0 < mr.nblk; b0 += 8) {
+        unsigned long long v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b0 + u < mr.nblk ? mr.m[b0 + u] : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          unsigned bits = row_bits(v[u], mr.shift);
+          while (bits) {
+            const int r = (__ffs(bits) - 1) >> 2;
+            bits &= bits - 1u;
+            col[slot * kPoolLd] = uint32_t(8 * (b0 + u) + r);
+            ++slot;
+          }
+        }
+      }
+      // 2. offsets -> positions (run table)
+      const int ci = int(c - c0);
+      if (ci < kEmitCells) {
+        const uint32_t* ro = sm.roff[ci];
+        const uint32_t* rp = sm.rpos[ci];
+        for (int i = 0; i < len; ++i) {
+          const uint32_t t = col[i * kPoolLd];
+          int r = 0;  // last run with offset <= t (ro[0] == 0; padding is 0xffffffff)
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1)
+            if (ro[r + step] <= t) r += step;
+          col[i * kPoolLd] = rp[r] + (t - ro[r]);
+        }
+      } else {  // more than kEmitCells cells in the window (tiny cells): global search
+        const int64_t rb = cell_runs[c];
+        const int nr = int(cell_runs[c + 1] - rb);
+        for (int i = 0; i < len; ++i)
+          col[i * kPoolLd] = run_position(runs, run_off, rb, nr, col[i * kPoolLd]);
+      }
+      // 3. positions -> original ids, 16 gathers in flight
+      for (int i0 = 0; i0 < len; i0 += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          v[u] = i0 + u < len ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (i0 + u < len) col[(i0 + u) * kPoolLd] = v[u];
+      }
+    }
+    __syncwarp();
+    pool_sort(pool, pooled ? len : 0);
+    __syncwarp();
+    const unsigned todo = __ballot_sync(0xffffffffu, pooled);
+    for (unsigned m = todo; m; m &= m - 1u) {
+      const int k = __ffs(m) - 1;
+      const int L = __shfl_sync(0xffffffffu, len, k);
+      const int64_t D = __shfl_sync(0xffffffffu, dst, k);
+#pragma unroll
+      for (int e0 = 0; e0 < kPoolSlots; e0 += 32)
+        if (e0 + lane < L) nbr[D + e0 + lane] = pool[(e0 + lane) * kPoolLd + k];
+    }
+  }
+}
+
+// Rows longer than kPoolSlots: warp per row.  Lanes take blocks, a warp scan of
+// the per-block hit counts places every candidate offset in ascending order at
+// the row's destination, offsets are mapped to original ids in place, and the
+// row is sorted there (warp bitonic <= kWarpSortMax, else listed for the CTA /
+// radix path).
+__global__ void __launch_bounds__(256)
+    long_rows_kernel(const unsigned long long* __restrict__ masks,
+                     const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
+                     const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
+                     const uint32_t* __restrict__ run_off, const int64_t* __restrict__ cell_cand,
+                     int64_t n_cells, const uint32_t* __restrict__ perm,
+                     const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
+                     const uint32_t* __restrict__ long_rows, const unsigned long long* n_long,
+                     uint32_t* __restrict__ big_rows, unsigned long long* n_big) {
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t nl = int64_t(*n_long);
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32; i < nl; i += warps) {
+    const uint32_t p = long_rows[i];
+    int64_t lo = 0, hi = n_cells;  // cell containing p
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cell_start[mid] <= p) lo = mid;
+      else hi = mid;
+    }
+    const int64_t c = lo;
+    const uint32_t id = perm[p];
+    const int64_t dst = offsets[id];
+    const int len = int(offsets[id + 1] - dst);
+    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, int64_t(p) - cell_start[c]);
+    uint32_t* row = nbr + dst;
+    int base = 0;
+    for (int b0 = 0; b0 < mr.nblk; b0 += 32) {
+      const int b = b0 + lane;
+      unsigned bits = b < mr.nblk ? row_bits(__ldg(mr.m + b), mr.shift) : 0u;
+      const int cnt = __popc(bits);
+      int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, ci, o);
-        if (lane >= o) ci += t;
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      const int poff = ci - cnt;
-      const bool pooled = poff + cnt <= kSliceBuf;
-      const int64_t dst = qa ? pos_off[cs + q0 + lane] : 0;  // row start, position order
-      __syncwarp();
-      if (qa) {
-        sm.dst[lane] = dst;
-        sm.slot[lane] = pooled ? uint32_t(poff) : 0u;
+      int at = base + incl - cnt;
+      while (bits) {
+        const int r = (__ffs(bits) - 1) >> 2;
+        bits &= bits - 1u;
+        row[at++] = uint32_t(8 * b + r);
       }
-      {
-        const unsigned dm = __ballot_sync(0xffffffffu, qa && !pooled);
-        if (lane == 0) sm.direct = dm;
-      }
-      for (int b0 = 0; b0 < total; b0 += kExpandBlk) {
-        const int nb = min(kExpandBlk, total - b0);
-        __syncwarp();
-        {
-          const int lo = max(myfirst, b0), hi = min(myfirst + mynblk, b0 + nb);
-          for (int b = lo; b < hi; ++b) sm.pos[b - b0] = myrun.x + 8u * uint32_t(b - myfirst);
-        }
-        __syncwarp();
-        // original ids of the chunk's candidates: 4 loads in flight per lane
-        for (int i0 = 0; i0 < nb * 8; i0 += 128) {
-          uint32_t v[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int i = i0 + 32 * k + lane;
-            const uint32_t p = i < nb * 8 ? sm.pos[i >> 3] + uint32_t(i & 7) : n_points;
-            v[k] = p < n_points ? __ldg(perm + p) : 0u;  // rows past a run end never hit
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int i = i0 + 32 * k + lane;
-            if (i < nb * 8) sm.ids[i] = v[k];
-          }
-        }
-        // the slice's mask words, split into halves and compacted to the non-empty ones
-        const int nw = nb * ngs;  // word w = (block w / ngs, group w % ngs)
-        int nunits = 0;
-        for (int i0 = 0; i0 < nw; i0 += 128) {
-          unsigned long long v[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int w = i0 + 32 * k + lane;
-            const int b = ngs == 3 ? int((unsigned(w) * 0xAAABu) >> 17) : (w >> (ngs >> 1));
-            v[k] = w < nw ? __ldg(mb + size_t(b0 + b) * ngc + gs + (w - b * ngs)) : 0ull;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int w = i0 + 32 * k + lane;
-            const int b = ngs == 3 ? int((unsigned(w) * 0xAAABu) >> 17) : (w >> (ngs >> 1));
-            const unsigned meta = (unsigned(8 * b) << 8) | unsigned(8 * (w - b * ngs));
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const unsigned bits = unsigned(v[k] >> (32 * h));
-              const unsigned bal = __ballot_sync(0xffffffffu, bits != 0u);
-              if (bits) sm.units[nunits + __popc(bal & lt)] = make_uint2(bits, meta + h);
-              nunits += __popc(bal);
-            }
-          }
-        }
-        if (lane == 0) sm.next = 32;
-        __syncwarp();
-        const unsigned direct = sm.direct;
-        int k = lane;
-        uint2 e = k < nunits ? sm.units[k] : make_uint2(0u, 0u);
-        while (__any_sync(0xffffffffu, k < nunits)) {
-          if (k < nunits) {
-            const int j = __ffs(e.x) - 1;
-            e.x &= e.x - 1u;
-            const int col = int(e.y & 0xffu) + 2 * (j & 3);
-            const uint32_t v = sm.ids[(e.y >> 8) + (j >> 2)];
-            const uint32_t slot = atomicAdd(&sm.slot[col], 1u);
-            if (!((direct >> col) & 1u)) sm.buf[slot] = v;
-            else rows_out[sm.dst[col] + slot] = v;
-            if (e.x == 0u) {
-              k = int(atomicAdd(&sm.next, 1u));
-              if (k < nunits) e = sm.units[k];
-            }
-          }
-        }
-      }
-      __syncwarp();
-      // the buffered rows (a prefix of the slice) are contiguous in rows_out too
-      int pend = (qa && pooled) ? poff + cnt : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) pend = max(pend, __shfl_xor_sync(0xffffffffu, pend, o));
-      const int64_t d0 = __shfl_sync(0xffffffffu, dst, 0);
-      for (int i = lane; i < pend; i += 32) rows_out[d0 + i] = sm.buf[i];
+      base += __shfl_sync(0xffffffffu, incl, 31);
     }
+    (void)lt;
+    __syncwarp();
+    const int64_t rb = cell_runs[c];
+    const int nr = int(cell_runs[c + 1] - rb);
+    for (int e = lane; e < len; e += 32) row[e] = perm[run_position(runs, run_off, rb, nr, row[e])];
+    __syncwarp();
+    sort_long_row(row, len, id, big_rows, n_big);
+  }
+}
+
+// win_cell[w] = the cell containing position 32 w.
+__global__ void window_cells_kernel(const int64_t* __restrict__ cell_start, int64_t n_cells,
+                                    uint32_t* __restrict__ win_cell) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cs = cell_start[c], ce = cell_start[c + 1];
+    for (int64_t w = (cs + 31) >> 5; (w << 5) < ce; ++w) win_cell[w] = uint32_t(c);
   }
 }
 
@@ -497,6 +622,23 @@ __global__ void huge_scatter_kernel(const int64_t* __restrict__ offsets, uint32_
 
 static unsigned blocks_for(int64_t n, int threads) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), kNumSMs * 16)));
+}
+
+void build_window_cells(tj_ctx* ctx, cudaStream_t s) {
+  const int64_t n_win = ceil_div(ctx->g.n, 32);
+  ctx->win_cell.ensure(sizeof(uint32_t) * std::max<int64_t>(n_win, 1), s);
+  window_cells_kernel<<<blocks_for(ctx->g.n_cells, 256), 256, 0, s>>>(
+      ctx->cell_start.as<int64_t>(), ctx->g.n_cells, ctx->win_cell.as<uint32_t>());
+  TJ_CHECK_LAUNCH();
+}
+
+void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
+                       cudaStream_t s) {
+  count_rows_kernel<<<kNumSMs * 8, 256, 0, s>>>(
+      ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
+      ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
+      ctx->win_cell.as<uint32_t>(), cb, ce, ctx->qcount.as<uint32_t>(), hits);
+  TJ_CHECK_LAUNCH();
 }
 
 // Sort the rows listed in big_rows (> kWarpSortMax ids) in place.
@@ -573,41 +715,54 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
   TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   if (n_pairs == 0 && n_mask_hits == 0) return;
 
-  // rows in cell (position) order first: offsets by position, then the ids
-  ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
-  int64_t* pos_off = ctx->pos_off.as<int64_t>();
-  scan_exclusive(LoadAt<uint32_t>{ctx->qcount.as<uint32_t>()}, StoreAt<int64_t>{pos_off}, n, sc, s);
-  TJ_CUDA(cudaMemcpyAsync(pos_off + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  const int64_t total = n_pairs + n_mask_hits;
-  ctx->rows_tmp.ensure(sizeof(uint32_t) * std::max<int64_t>(total, 1), s);
-  uint32_t* rows = ctx->rows_tmp.as<uint32_t>();
+  // `fill` doubles as the list of rows too long for the in-register sorts
   ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
   uint32_t* fill = ctx->fill.as<uint32_t>();
   unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
-  TJ_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
+  TJ_CUDA(cudaMemsetAsync(nbig, 0, 3 * sizeof(unsigned long long), s));
   if (n_mask_hits > 0) {
+    // low-d masks: short rows expanded, sorted and placed in one pass; long rows
+    // by a warp each
     const int64_t nc = ctx->g.n_cells;
-    const size_t smem = sizeof(ExpandSmem) * kExpandWarps;
-    TJ_CUDA(cudaFuncSetAttribute(expand_masks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    int per_sm = 0;
-    TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_masks_kernel,
-                                                          kExpandWarps * 32, smem));
-    const int64_t grid = std::min<int64_t>(ceil_div(nc, kExpandWarps),
-                                           int64_t(kNumSMs) * std::max(per_sm, 1));
-    expand_masks_kernel<<<unsigned(std::max<int64_t>(grid, 1)), kExpandWarps * 32, smem, s>>>(
+    const int64_t n_win = ceil_div(n, 32);
+    ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
+    uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
+    {
+      const size_t smem = sizeof(EmitSmem) * kEmitWarps;
+      TJ_CUDA(cudaFuncSetAttribute(emit_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+      int per_sm = 0;
+      TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_rows_kernel,
+                                                            kEmitWarps * 32, smem));
+      const int64_t grid = std::min<int64_t>(ceil_div(n_win, kEmitWarps),
+                                             int64_t(kNumSMs) * std::max(per_sm, 1));
+      emit_rows_kernel<<<unsigned(std::max<int64_t>(grid, 1)), kEmitWarps * 32, smem, s>>>(
+          ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
+          ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+          ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc,
+          ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
+          offsets, n, nbr, long_rows, nbig + 2);
+      TJ_CHECK_LAUNCH();
+    }
+    long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
-        ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(), nc,
-        ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(), pos_off, rows, uint32_t(n));
+        ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+        ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc, ctx->perm.as<uint32_t>(),
+        offsets, nbr, long_rows, nbig + 2, fill, nbig);
     TJ_CHECK_LAUNCH();
   } else {
+    // pair path: rows in cell (position) order first, then sorted into place
+    ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
+    int64_t* pos_off = ctx->pos_off.as<int64_t>();
+    scan_exclusive(LoadAt<uint32_t>{ctx->qcount.as<uint32_t>()}, StoreAt<int64_t>{pos_off}, n, sc,
+                   s);
+    TJ_CUDA(cudaMemcpyAsync(pos_off + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    ctx->rows_tmp.ensure(sizeof(uint32_t) * std::max<int64_t>(n_pairs, 1), s);
+    uint32_t* rows = ctx->rows_tmp.as<uint32_t>();
     TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
     scatter_pairs_kernel<<<blocks_for(n_pairs, 256), 256, 0, s>>>(
         ctx->pairs.as<uint2>(), n_pairs, ctx->perm.as<uint32_t>(), pos_off, fill, rows);
     TJ_CHECK_LAUNCH();
-  }
-  // sort each row into its final place; `fill` becomes the list of long rows
-  {
     const size_t smem = sizeof(uint32_t) * kPoolSlots * kPoolLd * kSortWarps;
     TJ_CUDA(cudaFuncSetAttribute(sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));

@@ -261,28 +261,24 @@ __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key,
 // Warp per cell: number of non-empty runs and candidates.
 __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
                                   const int64_t* __restrict__ cell_start, int64_t n_cells,
-                                  int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count,
-                                  int64_t* __restrict__ blk_count) {
+                                  int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count) {
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
     const uint64_t key = cell_key[c];
-    int64_t runs = 0, cands = 0, blks = 0;
+    int64_t runs = 0, cands = 0;
     for (int r = lane_id(); r < rp.n_rows; r += 32) {
       int64_t b, e;
       neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
       if (e > b) {
         runs += 1;
         cands += e - b;
-        blks += (e - b + 7) >> 3;
       }
     }
     runs = warp_sum(runs);
     cands = warp_sum(cands);
-    blks = warp_sum(blks);
     if (lane_id() == 0) {
       run_count[c] = runs;
       cand_count[c] = cands;
-      blk_count[c] = blks;  // 8-candidate blocks when every run is tiled on its own
     }
   }
 }
@@ -495,12 +491,10 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   ctx->cell_cost.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->tmp64.ensure(sizeof(int64_t) * (nc + 1), s);
   const unsigned warp_blocks = grid_for(nc * 32, 256);
-  ctx->cell_blocks.ensure(sizeof(int64_t) * (nc + 1), s);
   cand_count_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
                                                 ctx->cell_start.as<int64_t>(), nc,
                                                 ctx->tmp64.as<int64_t>(),
-                                                ctx->cell_cand.as<int64_t>(),
-                                                ctx->cell_blocks.as<int64_t>());
+                                                ctx->cell_cand.as<int64_t>());
   TJ_CHECK_LAUNCH();
   sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
   scan_exclusive(LoadAt<int64_t>{ctx->tmp64.as<int64_t>()},
@@ -589,14 +583,15 @@ __global__ void item_fill_kernel(const int64_t* __restrict__ cell_start,
 
 // Low-d hit masks: every (query group, 8-candidate block) tile of the cells
 // [cb, ce) owns one 64-bit mask.  Cell c's masks start at mbase[c - cb] and are
-// ordered (group, block) with blocks as in the refine kernel's run-by-run tiling.
+// ordered (group, block); block b = candidates [8b, 8b+8) of the concatenated
+// list, i.e. the reference's tiling (join.py:257-261).
 struct MaskCountIn {
   const int64_t* cell_start;
-  const int64_t* blocks;
+  const int64_t* cand;
   int64_t cb;
   __device__ int64_t operator()(int64_t i) const {
     const int64_t c = cb + i;
-    return ((cell_start[c + 1] - cell_start[c] + 7) / 8) * blocks[c];
+    return ((cell_start[c + 1] - cell_start[c] + 7) / 8) * ((cand[c] + 7) / 8);
   }
 };
 
@@ -605,7 +600,7 @@ int64_t build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
   if (n <= 0) return 0;
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
   ctx->cell_mbase.ensure(sizeof(int64_t) * (n + 1), s);
-  scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_blocks.as<int64_t>(), cb},
+  scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb},
                  StoreAt<int64_t>{ctx->cell_mbase.as<int64_t>()}, n, sc, s);
   return read_scalar<int64_t>(sc.total, s);
 }

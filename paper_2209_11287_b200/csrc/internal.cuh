@@ -89,7 +89,6 @@ struct RefineArgs {
   uint32_t* qcount;        // (n) per-query pair counts (cell-ordered positions)
   unsigned long long* masks;     // low-d hit masks
   const int64_t* cell_mbase;     // first mask of cell c at cell_mbase[c - cell_base]
-  const int64_t* cell_blocks;    // 8-candidate blocks per cell (runs tiled separately)
   int64_t cell_base;
   int d, d_pad, nchunks;
   double eps_sq;
@@ -123,7 +122,7 @@ struct tj_ctx {
   // scratch
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
   // results
-  tj::DevBuf pairs, qcount, counters, fill, masks, cell_blocks, cell_mbase;
+  tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
   unsigned long long pair_cap = 0;
   int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
@@ -149,11 +148,15 @@ int64_t build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cuda
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
 void launch_refine_tc(const RefineArgs& a, cudaStream_t s);  // DMMA, 5 <= d <= 64
-void launch_refine_lowd(const RefineArgs& a, cudaStream_t s);  // d <= 4, unsliced items
-int lowd_queries_per_item();
+void launch_refine_lowd(const RefineArgs& a, int64_t n, int64_t n_cells,
+                        cudaStream_t s);  // d <= 4, unsliced items
+int lowd_queries_per_item(int64_t n, int64_t n_cells);
 int core_queries_per_item(int d, int d_pad);
 int tc_queries_per_item(int d_pad);
 // finalize.cu
+void build_window_cells(tj_ctx* ctx, cudaStream_t s);
+void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
+                       cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
                   int64_t n_mask_hits, cudaStream_t s);
 }  // namespace tj
