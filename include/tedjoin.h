@@ -126,6 +126,44 @@ int tj_get_stats(tj_ctx* ctx, tj_stats* out);
  * (join.py:114-147) and the multi-GPU cost-balanced cell split. */
 int tj_cell_costs(tj_ctx* ctx, int64_t* costs);
 
+/* ---- callers either side of the path --------------------- */
+/* Canonical squared distance of every emitted pair, for the pairs file
+ * (cli._canonical_pair_sq_dists + _write_pairs, cli.py:270-289): out[e] = the
+ * direct form sum over ascending dims of fl(fl(x_i - x_j)^2) for the e-th pair
+ * (i, neighbors[e]) of the CSR.  coords: device, original point order, row
+ * stride ld; offsets: device int64[n+1]; neighbors: device uint32[m]; out:
+ * device double[m].  Asynchronous. */
+int tj_pair_sq_dists(tj_ctx* ctx, const double* coords, int64_t ld, int32_t d,
+                     const int64_t* offsets, int64_t n, const uint32_t* neighbors, int64_t m,
+                     double* out, void* stream);
+
+/* Write the pairs file: one "i j sq" line per CSR pair, sq formatted like
+ * Python's f"{sq:.17g}" (cli._write_pairs, cli.py:285-289).  All pointers are
+ * host arrays (offsets int64[n+1], neighbors uint32[offsets[n]], sq double[..]);
+ * `threads` host threads format blocks in parallel.  Synchronous. */
+int tj_write_pairs(const char* path, const int64_t* offsets, int64_t n,
+                   const uint32_t* neighbors, const double* sq, int32_t threads);
+
+/* Per-column mean and variance of coords (device, n rows, stride ld, first d
+ * columns) into host arrays mean[d], var[d] (synchronous).  Feeds the variance
+ * dimension reordering (datasets.reorder_dims_by_variance, datasets.py:113-123);
+ * compensated summation: accurate to a few ulp, order-independent. */
+int tj_column_moments(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                      double* mean, double* var, void* stream);
+/* dst[:, j] = src[:, perm[j]] for j < d, zero for d <= j < ld_out.  src/dst
+ * device (distinct buffers), perm host int32[d].  Synchronous. */
+int tj_permute_columns(tj_ctx* ctx, const double* src, int64_t n, int32_t d, int64_t ld,
+                       const int32_t* perm, double* dst, int64_t ld_out, void* stream);
+
+/* Brute-force self-join over all n^2 ordered pairs with the reference direct
+ * form (oracle.brute_force_join, oracle.py:55-86): the GPU verification oracle
+ * of cli verify for n beyond the CPU guard.  Two calls: with neighbors == NULL
+ * it fills offsets (device int64[n+1]) and *total (host); then with a device
+ * uint32[*total] buffer it writes the rows (ascending).  d <= 128. */
+int tj_brute_force(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                   double eps, int64_t* offsets, uint32_t* neighbors, int64_t* total,
+                   void* stream);
+
 /* ---- measurement helpers ------------------------------------------------ */
 /* FP64 throughput microbenchmark on the current device: kind 0 = DFMA,
  * 1 = DMMA m8n8k4, 2 = both interleaved.  Reports FLOP/s counting 2 per FMA. */

@@ -6,7 +6,15 @@ Drop-in for the self-join path of the reference package `tilejoin`
 sm_100a CUDA (libtedjoin.so) behind a C ABI (include/tedjoin.h).
 """
 
-from .datasets import Dataset, GenSpec, as_dataset, generate, reorder_dims_by_variance
+from .datasets import (
+    Dataset,
+    GenSpec,
+    as_dataset,
+    generate,
+    read_dataset,
+    reorder_dims_by_variance,
+    write_dataset,
+)
 from .errors import BoundsError, ParseError, ResourceError, ValidationError
 from .join import (
     BatchPlan,
@@ -25,5 +33,6 @@ __version__ = "0.1.0"
 __all__ = [
     "BatchPlan", "BoundsError", "Dataset", "GenSpec", "JoinConfig", "JoinResult", "JoinStats",
     "ParseError", "ResourceError", "ValidationError", "as_dataset", "generate", "join_stats",
-    "plan_batches", "plan_from_estimates", "reorder_dims_by_variance", "selectivity", "self_join",
+    "plan_batches", "plan_from_estimates", "read_dataset", "reorder_dims_by_variance",
+    "selectivity", "self_join", "write_dataset",
 ]

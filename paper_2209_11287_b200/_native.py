@@ -56,6 +56,11 @@ SIGNATURES = {
     "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_get_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
     "tj_cell_costs": (_i32, [_vp, _vp]),
+    "tj_pair_sq_dists": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "tj_write_pairs": (_i32, [ctypes.c_char_p, _vp, _i64, _vp, _vp, _i32]),
+    "tj_column_moments": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _vp]),
+    "tj_permute_columns": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _i64, _vp]),
+    "tj_brute_force": (_i32, [_vp, _vp, _i64, _i32, _i64, _f64, _vp, _vp, _vp, _vp]),
     "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
     "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_last_refine_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
@@ -190,6 +195,42 @@ class Context:
         self._check(self.lib.tj_get_stats(self.handle, ctypes.byref(st)))
         return st
 
+    def pair_sq_dists(self, coords, d: int, offsets, neighbors, m: int, out, stream=None):
+        """Canonical direct-form squared distance of every CSR pair (device tensors)."""
+        s = stream or self.stream()
+        n = offsets.shape[0] - 1
+        self._check(self.lib.tj_pair_sq_dists(
+            self.handle, coords.data_ptr(), int(coords.stride(0)), int(d), offsets.data_ptr(), n,
+            neighbors.data_ptr() if m else None, int(m), out.data_ptr() if m else None,
+            s.cuda_stream))
+
+    def column_moments(self, coords, n: int, d: int):
+        """(mean, var) numpy arrays of the first d columns of a device tensor."""
+        import numpy as np
+
+        mean, var = np.empty(d), np.empty(d)
+        self._check(self.lib.tj_column_moments(self.handle, coords.data_ptr(), int(n), int(d),
+                                               int(coords.stride(0)), mean.ctypes.data,
+                                               var.ctypes.data, self.stream().cuda_stream))
+        return mean, var
+
+    def permute_columns(self, src, n: int, d: int, perm, dst):
+        import numpy as np
+
+        p = np.ascontiguousarray(perm, dtype=np.int32)
+        self._check(self.lib.tj_permute_columns(self.handle, src.data_ptr(), int(n), int(d),
+                                                int(src.stride(0)), p.ctypes.data, dst.data_ptr(),
+                                                int(dst.stride(0)), self.stream().cuda_stream))
+
+    def brute_force(self, coords, n: int, d: int, eps: float, offsets, neighbors=None):
+        """Two-phase GPU brute force: without neighbors returns the pair count."""
+        total = _i64()
+        self._check(self.lib.tj_brute_force(
+            self.handle, coords.data_ptr(), int(n), int(d), int(coords.stride(0)), float(eps),
+            offsets.data_ptr(), neighbors.data_ptr() if neighbors is not None else None,
+            ctypes.byref(total) if neighbors is None else None, self.stream().cuda_stream))
+        return int(total.value)
+
     def last_refine_ms(self) -> float:
         ms = _f64()
         self._check(self.lib.tj_last_refine_ms(self.handle, ctypes.byref(ms)))
@@ -211,6 +252,21 @@ def context(device: int | None = None) -> Context:
         if ctx is None:
             ctx = _contexts[dev] = Context(dev)
         return ctx
+
+
+def write_pairs(path, offsets, neighbors, sq, threads: int | None = None) -> None:
+    """Pairs file from host CSR arrays + squared distances (native, multi-threaded)."""
+    import numpy as np
+
+    lib = load_library()
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    nb = np.ascontiguousarray(neighbors, dtype=np.uint32)
+    sq = np.ascontiguousarray(sq, dtype=np.float64)
+    th = threads or min(16, os.cpu_count() or 1)
+    st = lib.tj_write_pairs(os.fsencode(os.fspath(path)), off.ctypes.data, len(off) - 1,
+                            nb.ctypes.data, sq.ctypes.data, int(th))
+    if st != TJ_OK:
+        _raise(st, lib.tj_last_error(None).decode())
 
 
 def launch_count() -> int:

@@ -399,4 +399,57 @@ int tj_cell_costs(tj_ctx* ctx, int64_t* costs) {
   });
 }
 
+int tj_pair_sq_dists(tj_ctx* ctx, const double* coords, int64_t ld, int32_t d,
+                     const int64_t* offsets, int64_t n, const uint32_t* neighbors, int64_t m,
+                     double* out, void* stream) {
+  if (!ctx || !coords || !offsets || (m > 0 && (!neighbors || !out))) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (d < 1 || ld < d || n < 0 || m < 0) fail(TJ_EINVAL, "need d >= 1, ld >= d, n, m >= 0");
+    launch_pair_sq_dists(coords, ld, d, offsets, n, neighbors, m, out,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_write_pairs(const char* path, const int64_t* offsets, int64_t n,
+                   const uint32_t* neighbors, const double* sq, int32_t threads) {
+  if (!path || !offsets || n < 0) return TJ_EINVAL;
+  return guarded(nullptr, [&] {
+    if (offsets[n] > 0 && (!neighbors || !sq)) fail(TJ_EINVAL, "neighbors / sq is null");
+    write_pairs_file(path, offsets, n, neighbors, sq, threads);
+  });
+}
+
+int tj_column_moments(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                      double* mean, double* var, void* stream) {
+  if (!ctx || !coords || !mean || !var) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (n < 1 || d < 1 || ld < d) fail(TJ_EINVAL, "need n >= 1, d >= 1, ld >= d");
+    column_moments(ctx, coords, n, d, ld, mean, var, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_permute_columns(tj_ctx* ctx, const double* src, int64_t n, int32_t d, int64_t ld,
+                       const int32_t* perm, double* dst, int64_t ld_out, void* stream) {
+  if (!ctx || !src || !perm || !dst) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (n < 1 || d < 1 || ld < d || ld_out < d) fail(TJ_EINVAL, "need n, d >= 1, ld, ld_out >= d");
+    for (int j = 0; j < d; ++j)
+      if (perm[j] < 0 || perm[j] >= d) fail(TJ_EINVAL, "perm entries must be in [0, d)");
+    permute_columns(src, n, d, ld, perm, dst, ld_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_brute_force(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
+                   double eps, int64_t* offsets, uint32_t* neighbors, int64_t* total,
+                   void* stream) {
+  if (!ctx || !coords || !offsets || (!neighbors && !total)) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (n < 1 || d < 1 || ld < d) fail(TJ_EINVAL, "need n >= 1, d >= 1, ld >= d");
+    if (!(std::isfinite(eps) && eps > 0)) fail(TJ_EINVAL, "epsilon must be positive and finite");
+    if (n >= (int64_t(1) << 32) - 1) fail(TJ_EINVAL, "n must be < 2^32 - 1 (32-bit point ids)");
+    brute_force_join(ctx, coords, n, d, ld, eps, offsets, neighbors, total,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
 }  // extern "C"

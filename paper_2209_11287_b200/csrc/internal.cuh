@@ -154,6 +154,17 @@ int lowd_queries_per_item(int64_t n, int64_t n_cells);
 int core_queries_per_item(int d, int d_pad);
 int tc_queries_per_item(int d_pad);
 // finalize.cu
+// output.cu / reorder.cu / verify.cu
+void launch_pair_sq_dists(const double* x, int64_t ld, int d, const int64_t* offsets, int64_t n,
+                          const uint32_t* nbr, int64_t m, double* out, cudaStream_t s);
+void write_pairs_file(const char* path, const int64_t* offsets, int64_t n, const uint32_t* nbr,
+                      const double* sq, int threads);
+void column_moments(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld, double* h_mean,
+                    double* h_var, cudaStream_t s);
+void permute_columns(const double* src, int64_t n, int d, int64_t ld, const int* h_perm,
+                     double* dst, int64_t ld_out, cudaStream_t s);
+void brute_force_join(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld, double eps,
+                      int64_t* offsets, uint32_t* nbr, int64_t* total, cudaStream_t s);
 void build_window_cells(tj_ctx* ctx, cudaStream_t s);
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
                        cudaStream_t s);

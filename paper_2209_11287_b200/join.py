@@ -344,6 +344,31 @@ class DeviceJoin:
         return s
 
 
+# Variances closer than this (relative) are re-ranked on the host with numpy's own
+# var(axis=0): compensated device sums are accurate to a few ulp, numpy's
+# sequential ones to ~n ulp, so only such near-ties could order differently.
+_VAR_TIE_REL = 1e-8
+
+
+def variance_order(ctx, coords, dataset: Dataset) -> np.ndarray:
+    """np.argsort(-var, kind="stable") of the columns (datasets.py:119-122), var on the GPU."""
+    _, var = ctx.column_moments(coords, dataset.n, dataset.d)
+    v = np.sort(var)
+    if dataset.d > 1 and np.any(np.diff(v) <= _VAR_TIE_REL * np.abs(v[1:])):
+        var = dataset.logical.var(axis=0)  # near-tie: the reference's exact values decide
+    return np.argsort(-var, kind="stable")
+
+
+def reorder_dims_on_device(ctx, coords, dataset: Dataset):
+    """Device copy of the coordinates with columns in non-increasing variance order."""
+    perm = variance_order(ctx, coords, dataset)
+    if np.array_equal(perm, np.arange(dataset.d)):
+        return coords
+    out = coords.new_empty(coords.shape)
+    ctx.permute_columns(coords, dataset.n, dataset.d, perm, out)
+    return out
+
+
 def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) -> JoinResult:
     """Find every ordered pair within config.epsilon, self-pairs included (join.py:150-215).
 
@@ -353,11 +378,11 @@ def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) 
     t_start = time.perf_counter()
     dataset = as_dataset(dataset)
     _validate_config(config)
-    work = dataset
-    if config.reorder_dims and dataset.n >= 2:
-        work, _ = reorder_dims_by_variance(dataset)
-    job = DeviceJoin(work, config)
-    job.build()
+    job = DeviceJoin(dataset, config)
+    coords = upload(dataset, job.device)
+    if config.reorder_dims and dataset.n >= 2:  # join.py:163-164, on the device
+        coords = reorder_dims_on_device(job.ctx, coords, dataset)
+    job.build(coords)
     t_indexed = time.perf_counter()
     total = job.refine(max_result_pairs=max_result_pairs)
     job.finalize()
