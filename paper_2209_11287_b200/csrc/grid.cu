@@ -145,25 +145,17 @@ __global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, 
   if (lane_id() == 0) atomicMax(max_norm_bits, local_max);
 }
 
-// Short-circuit suffixes (d > 4): SFX[p][c] = sum of p's chunk norms after check
-// point c, check points after chunks CE-1, 2CE-1, ... (CE = ceil(nchunks/4)).
-// SFX[p][3] = |p|^2, so one 32-byte record carries everything a DMMA tile needs
-// besides the coordinates.
+// Short-circuit record (d > 4): SFX[p] = (sum of p's chunk norms from chunk
+// nchunks/2 on, |p|^2) -- the one 16-byte record a DMMA tile needs besides the
+// coordinates (the check point sits after half of the chunks, refine_tc.cu).
 __global__ void suffix_kernel(const double* __restrict__ CN, const double* __restrict__ NRM,
                               int64_t n, int nchunks, double* __restrict__ SFX) {
-  const int ce = (nchunks + 3) / 4;
-  const int ncheck = (nchunks - 1) / ce;
+  const int ch = nchunks / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
        p += int64_t(gridDim.x) * blockDim.x) {
-    double s[4] = {0.0, 0.0, 0.0, NRM[p]};
-    for (int c = 0; c < ncheck && c < 3; ++c) {
-      double acc = 0.0;
-      for (int j = (c + 1) * ce; j < nchunks; ++j) acc += CN[p * nchunks + j];
-      s[c] = acc;
-    }
-    double2* dst = reinterpret_cast<double2*>(SFX + p * 4);
-    dst[0] = make_double2(s[0], s[1]);
-    dst[1] = make_double2(s[2], s[3]);
+    double acc = 0.0;
+    for (int j = ch; j < nchunks; ++j) acc += CN[p * nchunks + j];
+    reinterpret_cast<double2*>(SFX)[p] = make_double2(acc, NRM[p]);
   }
 }
 
@@ -450,7 +442,7 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
       ctx->NRM.as<double>(), reinterpret_cast<unsigned long long*>(mm + 2 * TJ_MAX_K_IDX));
   TJ_CHECK_LAUNCH();
   if (g.nchunks > 1) {
-    ctx->SFX.ensure(sizeof(double) * 4 * n, s);
+    ctx->SFX.ensure(sizeof(double) * 2 * n, s);
     suffix_kernel<<<grid_for(n, 256), 256, 0, s>>>(ctx->CN.as<double>(), ctx->NRM.as<double>(), n,
                                                     g.nchunks, ctx->SFX.as<double>());
     TJ_CHECK_LAUNCH();

@@ -76,7 +76,7 @@ struct RefineArgs {
   const double* P;         // (n, d_pad) cell-ordered coordinates
   const double* NRM;       // (n) squared norms (any rounding order; the guard covers it)
   const double* CN;        // (n, nchunks) chunk norms, reference order (kernels.py:126-130)
-  const double* SFX;       // (n, 4) chunk-norm suffixes after each short-circuit check point
+  const double* SFX;       // (n, 2): chunk-norm suffix after the short-circuit check, |c|^2
   const uint2* runs;       // (n_runs) candidate position ranges [begin, end)
   const uint32_t* run_off; // (n_runs) offset of each run inside its cell's concatenation
   const int64_t* cell_runs;   // (n_cells+1)

@@ -5,28 +5,31 @@
 // per 4-dim chunk D = (-2Q) * C^T + acc, short-circuit when every entry of the
 // tile already exceeds eps^2 (join.py:250-253), emit <= eps^2.
 //
-// B200 mapping (same ideas as refine_lowd.cu, generalised to several chunks):
-//  * one warp per work item (<= 8*NGM queries of one cell x a slice of its
-//    concatenated candidate list), transposed tiles: candidates are the A operand
-//    (rows), queries the B operand (columns, -2*q chunk fragments held in
-//    registers for the whole item), C starts at the candidate norm and the NCH
-//    DMMAs of a tile chain through the accumulator;
-//  * a warp-uniform cursor walks the item's runs (clipped to its slice) block by
-//    block; each 8-candidate block is staged into a per-warp shared-memory ring
-//    with cp.async using a fixed lane -> (row, 16-byte piece) map (no index
-//    division), rows padded so fragment reads are bank-conflict free; the 32-byte
-//    record (3 short-circuit suffixes + |c|^2) rides along;
-//  * short-circuit at up to 3 check points: a tile stops when every entry's
-//    partial distance (acc - candidate suffix + query prefix) exceeds
-//    eps^2 + 2*guard — safe under rounding, decisions stay exact.  The check costs
-//    FP64 issue slots, so a warp turns it off for the rest of an item when fewer
-//    than a quarter of its first checks prune;
-//  * exact decisions: guard band as in refine_lowd.cu (integer high-word screen,
-//    rare out-of-line direct-form recheck);
+// B200 mapping (FP64-pipe bound, so the loop is built around keeping the DMMA
+// pipe fed):
+//  * one warp per work item (<= 8*NG queries of one cell x a slice of its
+//    concatenated candidate list), transposed tiles: candidates are the A
+//    operand (rows), queries the B operand (columns; -2*q chunk fragments stay
+//    in registers for the whole item), C starts at the candidate norm and the
+//    NCH DMMAs of a tile chain through the accumulator;
+//  * a warp-uniform cursor walks the item's runs (clipped to its slice) and
+//    cuts them into 8-candidate blocks; SB blocks form one stage of a per-warp
+//    cp.async ring (one wait + one barrier per stage, not per block); rows are
+//    padded so fragment reads are bank-conflict free; a 16-byte record per row
+//    (short-circuit suffix, |c|^2) rides along;
+//  * two blocks per step: 2 * NG independent DMMA chains are interleaved chunk
+//    by chunk, so the chain latency is hidden inside the warp;
+//  * short-circuit (optional, adaptive): one check after half of the chunks; a
+//    tile stops when every entry's partial distance (acc - candidate suffix +
+//    query prefix) exceeds eps^2 + 2*guard -- safe under rounding, decisions
+//    stay exact.  A warp stops checking for the rest of an item when fewer than
+//    a quarter of its first checks prune;
+//  * exact decisions: guard band as in refine_lowd.cu (values above the band's
+//    lower edge re-decided out of line by the reference direct form);
 //  * emission: hits are sparse at these dimensionalities (|R|/C ~ 1e-3), so
-//    pairs go through a per-warp shared-memory buffer flushed with one atomicAdd
-//    per 256 pairs; per-query counts accumulate in registers and are added once
-//    per item (items of a big cell share queries).
+//    pairs go through a per-warp shared-memory buffer flushed with one
+//    atomicAdd per 256 pairs; per-query counts accumulate in registers and are
+//    added once per item (items of a big cell share queries).
 #include "internal.cuh"
 #include "refine_common.cuh"
 
@@ -34,27 +37,27 @@ namespace tj {
 
 constexpr int kTcWarps = 4;
 constexpr int kTcThreads = kTcWarps * kWarp;
-constexpr int kTcStages = 4;  // blocks in the per-warp ring
+constexpr int kTcStages = 3;  // stages in the per-warp ring
 
 template <int NCH>
 struct TcShape {
   static constexpr int DP = 4 * NCH;
   static constexpr int STRIDE = (DP % 8 == 0) ? DP + 4 : DP;  // conflict-free fragment rows
-  static constexpr int NGM = NCH <= 8 ? 2 : 1;                 // query groups per item
-  static constexpr int CE = (NCH + 3) / 4;                     // chunks per check interval
-  static constexpr int NCHECK = (NCH - 1) / CE;                // check points (<= 3)
+  static constexpr int NG = NCH <= 8 ? 2 : 1;                  // query groups per item
+  static constexpr int SB = NCH <= 4 ? 4 : 2;                  // blocks per stage (even)
+  static constexpr int ROWS = 8 * SB;
   static constexpr int PPR = DP / 2;                           // 16-byte pieces per row
+  static constexpr int CH = NCH / 2;                           // chunks before the check
 };
 
 template <int NCH>
-struct alignas(16) TcBlock {
-  double pts[8][TcShape<NCH>::STRIDE];
-  double rec[8][4];  // suffixes after check points 0..2, |c|^2
-  uint32_t pos;      // position of row 0
+struct alignas(16) TcStage {
+  double pts[TcShape<NCH>::ROWS][TcShape<NCH>::STRIDE];
+  double rec[TcShape<NCH>::ROWS][2];  // chunk-norm suffix after the check point, |c|^2
+  uint32_t pos[TcShape<NCH>::SB];     // position of each block's row 0
+  uint32_t nblk;                      // blocks staged (the rest are padding)
   uint32_t pad[3];
 };
-
-__device__ __forceinline__ unsigned tc_hi_word(double v) { return unsigned(__double2hiint(v)); }
 
 __device__ __forceinline__ void tc_cp16(void* smem, const void* gmem) {
   const unsigned s = unsigned(__cvta_generic_to_shared(smem));
@@ -68,8 +71,9 @@ __device__ __forceinline__ void tc_wait() {
 
 // Re-decide guard-band pairs with the reference direct form (rare, out of line).
 __device__ __noinline__ uint2 tc_recheck(const double* P, int dp, int d, double eps_sq, bool b0,
-                                         bool b1, bool p0, bool p1, uint32_t qa, uint32_t c,
-                                         unsigned long long* ctr) {
+                                         bool b1, unsigned m0, unsigned m1, uint32_t qa,
+                                         uint32_t c, unsigned long long* ctr) {
+  bool p0 = (m0 >> lane_id()) & 1u, p1 = (m1 >> lane_id()) & 1u;
   if (b0) p0 = direct_form_le(P, dp, d, qa, c, eps_sq);
   if (b1) p1 = direct_form_le(P, dp, d, qa + 1, c, eps_sq);
   const unsigned nb = __popc(__ballot_sync(0xffffffffu, b0)) + __popc(__ballot_sync(0xffffffffu, b1));
@@ -78,7 +82,8 @@ __device__ __noinline__ uint2 tc_recheck(const double* P, int dp, int d, double 
 }
 
 // Warp-uniform walk over the item's runs clipped to [s0, s1) of the
-// concatenated candidate list, one 8-candidate block at a time.
+// concatenated candidate list, one 8-candidate block at a time (runs are tiled
+// separately: a block never straddles two runs, so its rows are contiguous).
 struct BlockCursor {
   int64_t r, re;     // current run, end of the cell's runs
   uint32_t x, y;     // remaining positions [x, y) of the current run piece
@@ -115,17 +120,124 @@ struct BlockCursor {
 };
 
 template <int NCH>
-__global__ void __launch_bounds__(kTcThreads, 4) refine_tc_kernel(RefineArgs a) {
+struct TcQuery {
+  static constexpr int NG = TcShape<NCH>::NG;
+  double bq[NG][NCH];  // -2 * query chunk, B fragments
+  double thr[NG][2];   // pass iff D <= thr (upper edge of the guard band)
+  double tlo[NG][2];   // D > tlo: inside the band, decided exactly
+  double pre[NG][2];   // check: prune iff D_partial - suffix > pre for the whole tile
+};
+
+// One step: blocks k and k+1 of stage s (the second may be padding) against
+// the NG query groups -- 2*NG accumulator chains advanced chunk by chunk.
+template <int NCH, bool SC>
+__device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH>& qs,
+                                        const TcStage<NCH>* s, int k, uint32_t q0, bool& check,
+                                        unsigned& n_checks, unsigned& n_pruned,
+                                        unsigned long long& st_skip, unsigned (&qc)[TcShape<NCH>::NG][2],
+                                        HitBuffer& hb, uint2* hits) {
   using S = TcShape<NCH>;
-  constexpr int DP = S::DP, NGM = S::NGM, CE = S::CE, NCHECK = S::NCHECK, PPR = S::PPR;
+  constexpr int NG = S::NG, CH = S::CH;
+  const int lane = lane_id();
+  const int row = lane >> 2, col = lane & 3;
+  const unsigned lt = lanemask_lt();
+  double acc[2][NG][2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const double cn = s->rec[8 * (k + u) + row][1];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) acc[u][g][0] = acc[u][g][1] = cn;
+  }
+  bool live[2][NG];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) live[u][g] = true;
+  // chunks [0, CH): all chains
+#pragma unroll
+  for (int j = 0; j < (SC ? CH : NCH); ++j) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double av = s->pts[8 * (k + u) + row][4 * j + col];
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        dmma_8x8x4(acc[u][g][0], acc[u][g][1], av, qs.bq[g][j], acc[u][g][0], acc[u][g][1]);
+    }
+  }
+  if constexpr (SC) {
+    if (check) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double sf = s->rec[8 * (k + u) + row][0];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const bool far = (acc[u][g][0] - sf > qs.pre[g][0]) && (acc[u][g][1] - sf > qs.pre[g][1]);
+          live[u][g] = !__all_sync(0xffffffffu, far);
+          ++n_checks;
+          if (!live[u][g]) {
+            ++n_pruned;
+            st_skip += NCH - CH;
+          }
+        }
+      }
+    }
+    // chunks [CH, NCH): chains still live
+#pragma unroll
+    for (int j = CH; j < NCH; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double av = s->pts[8 * (k + u) + row][4 * j + col];
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+          if (live[u][g])
+            dmma_8x8x4(acc[u][g][0], acc[u][g][1], av, qs.bq[g][j], acc[u][g][0], acc[u][g][1]);
+      }
+    }
+  }
+  // epilogue: compare + ballot; hits are rare
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      if (!live[u][g]) continue;
+      const bool p0 = acc[u][g][0] <= qs.thr[g][0];
+      const bool p1 = acc[u][g][1] <= qs.thr[g][1];
+      unsigned m0 = __ballot_sync(0xffffffffu, p0);
+      unsigned m1 = __ballot_sync(0xffffffffu, p1);
+      if ((m0 | m1) == 0) continue;
+      const uint32_t cpos = s->pos[k + u] + uint32_t(row);
+      const uint32_t qa = q0 + 8 * g + 2 * col;
+      const bool b0 = p0 && acc[u][g][0] > qs.tlo[g][0];
+      const bool b1 = p1 && acc[u][g][1] > qs.tlo[g][1];
+      if (__any_sync(0xffffffffu, b0 || b1)) {
+        const uint2 m = tc_recheck(a.P, 4 * NCH, a.d, a.eps_sq, b0, b1, m0, m1, qa, cpos,
+                                   &a.ctr->rechecks);
+        m0 = m.x;
+        m1 = m.y;
+        if ((m0 | m1) == 0) continue;
+      }
+      const bool h0 = (m0 >> lane) & 1u, h1 = (m1 >> lane) & 1u;
+      const int n0 = __popc(m0), n1 = __popc(m1);
+      hb.reserve(n0 + n1, hits, a);
+      if (h0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
+      if (h1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
+      hb.count += n0 + n1;
+      qc[g][0] += h0;
+      qc[g][1] += h1;
+    }
+}
+
+template <int NCH, bool SC>
+__global__ void __launch_bounds__(kTcThreads) refine_tc_kernel(RefineArgs a) {
+  using S = TcShape<NCH>;
+  constexpr int DP = S::DP, NG = S::NG, SB = S::SB, ROWS = S::ROWS, PPR = S::PPR, CH = S::CH;
   constexpr int R = kTcStages;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
-  const unsigned lt = lanemask_lt();
-  TcBlock<NCH>* ring = reinterpret_cast<TcBlock<NCH>*>(smem_raw) + warp * R;
-  uint2* hits = reinterpret_cast<uint2*>(reinterpret_cast<TcBlock<NCH>*>(smem_raw) + kTcWarps * R) +
+  TcStage<NCH>* ring = reinterpret_cast<TcStage<NCH>*>(smem_raw) + warp * R;
+  uint2* hits = reinterpret_cast<uint2*>(reinterpret_cast<TcStage<NCH>*>(smem_raw) + kTcWarps * R) +
                 warp * kHitBuf;
   HitBuffer hb;
   unsigned long long st_tiles_ref = 0, st_tiles = 0, st_skip = 0;
@@ -141,17 +253,14 @@ __global__ void __launch_bounds__(kTcThreads, 4) refine_tc_kernel(RefineArgs a) 
     const int ng = (nq + 7) >> 3;
 
     // ---- query side
-    double bq[NGM][NCH];
-    double thr[NGM][2];
-    unsigned h1[NGM][2], hw[NGM][2];
-    double qpre[NGM][NCHECK > 0 ? NCHECK : 1][2];
+    TcQuery<NCH> qs;
 #pragma unroll
-    for (int g = 0; g < NGM; ++g) {
+    for (int g = 0; g < NG; ++g) {
       const int qb = 8 * g + row;
       const bool vb = qb < nq;
 #pragma unroll
       for (int j = 0; j < NCH; ++j)
-        bq[g][j] = vb ? -2.0 * a.P[size_t(it.q0 + qb) * DP + 4 * j + col] : 0.0;
+        qs.bq[g][j] = vb ? -2.0 * a.P[size_t(it.q0 + qb) * DP + 4 * j + col] : 0.0;
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
         const int q = 8 * g + 2 * col + jj;
@@ -160,31 +269,17 @@ __global__ void __launch_bounds__(kTcThreads, 4) refine_tc_kernel(RefineArgs a) 
         const double qn = v ? a.NRM[qp] : 0.0;
         const double guard = a.guard_rel * (qn + a.max_norm) + 1e-300;
         const double center = eps_sq - qn;
-        const double hi = center + guard, lo = center - guard;
-        thr[g][jj] = v ? hi : -INFINITY;
-        if (!v) {
-          h1[g][jj] = 0u;
-          hw[g][jj] = 0u;
-        } else if ((hi < 0.0) == (lo < 0.0) && lo != 0.0 && hi != 0.0) {
-          const unsigned a1 = tc_hi_word(hi), a2 = tc_hi_word(lo);
-          h1[g][jj] = min(a1, a2);
-          hw[g][jj] = max(a1, a2) - min(a1, a2);
-        } else {
-          h1[g][jj] = 0u;
-          hw[g][jj] = 0xffffffffu;
-        }
-        // eps^2 + 2*guard - (query chunk norms up to each check point)
-#pragma unroll
-        for (int c = 0; c < NCHECK; ++c) {
-          double pre = 0.0;
-          for (int j = 0; j < (c + 1) * CE; ++j) pre += v ? a.CN[qp * NCH + j] : 0.0;
-          qpre[g][c][jj] = v ? eps_sq + 2.0 * guard - pre : -INFINITY;
-        }
+        qs.thr[g][jj] = v ? center + guard : -INFINITY;
+        qs.tlo[g][jj] = v ? center - guard : INFINITY;
+        // eps^2 + 2*guard - (query chunk norms up to the check point)
+        double pre = 0.0;
+        for (int j = 0; j < CH; ++j) pre += v ? a.CN[qp * NCH + j] : 0.0;
+        qs.pre[g][jj] = v ? eps_sq + 2.0 * guard - pre : -INFINITY;
       }
     }
-    unsigned qc[NGM][2];
+    unsigned qc[NG][2];
 #pragma unroll
-    for (int g = 0; g < NGM; ++g) qc[g][0] = qc[g][1] = 0;
+    for (int g = 0; g < NG; ++g) qc[g][0] = qc[g][1] = 0;
     st_tiles_ref += uint64_t(ng) * ((it.s1 - it.s0 + 7) >> 3);
 
     // ---- candidate stream
@@ -202,108 +297,81 @@ __global__ void __launch_bounds__(kTcThreads, 4) refine_tc_kernel(RefineArgs a) 
       cur.s1 = it.s1;
       cur.load_run(a);
     }
-    // stage one block into slot s: lane -> (row, piece) fixed map
-    auto issue = [&](TcBlock<NCH>* blk) -> bool {
-      uint32_t pos = 0, valid = 0;
-      const bool any = cur.next(pos, valid, a);
-      constexpr int RPI = 32 / PPR > 0 ? 32 / PPR : 1;  // rows per pass
+    // stage up to SB blocks; lane -> (row, 16-byte piece) over the whole stage
+    auto issue = [&](TcStage<NCH>* st) -> int {
+      uint32_t bpos[SB], bval[SB];
+      int nb = 0;
 #pragma unroll
-      for (int r0 = 0; r0 < 8; r0 += (PPR >= 32 ? 1 : RPI)) {
+      for (int b = 0; b < SB; ++b) {
+        bpos[b] = 0;
+        bval[b] = 0;
+        if (cur.next(bpos[b], bval[b], a)) ++nb;
+      }
 #pragma unroll
-        for (int p0 = 0; p0 < PPR; p0 += 32) {
-          const int rr = r0 + (PPR >= 32 ? 0 : lane / PPR);
-          const int pc = p0 + (PPR >= 32 ? lane : lane % PPR);
-          if (rr < 8 && pc < PPR) {
-            if (uint32_t(rr) < valid)
-              tc_cp16(&blk->pts[rr][2 * pc], a.P + size_t(pos + rr) * DP + 2 * pc);
-            else
-              *reinterpret_cast<double2*>(&blk->pts[rr][2 * pc]) = make_double2(0.0, 0.0);
-          }
+      for (int i0 = 0; i0 < ROWS * PPR; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < ROWS * PPR) {
+          const int rr = i / PPR, pc = i - rr * PPR;
+          const int b = rr >> 3, r8 = rr & 7;
+          uint32_t p = bpos[0], v = bval[0];
+#pragma unroll
+          for (int bb = 1; bb < SB; ++bb)
+            if (b == bb) {
+              p = bpos[bb];
+              v = bval[bb];
+            }
+          if (uint32_t(r8) < v) tc_cp16(&st->pts[rr][2 * pc], a.P + size_t(p + r8) * DP + 2 * pc);
+          else *reinterpret_cast<double2*>(&st->pts[rr][2 * pc]) = make_double2(0.0, 0.0);
         }
       }
-      if (lane < 16) {  // 8 records x 2 pieces
-        const int rr = lane >> 1, pc = lane & 1;
-        if (uint32_t(rr) < valid)
-          tc_cp16(&blk->rec[rr][2 * pc], a.SFX + size_t(pos + rr) * 4 + 2 * pc);
-        else
-          *reinterpret_cast<double2*>(&blk->rec[rr][2 * pc]) =
-              make_double2(pc ? 0.0 : 0.0, pc ? kPadNorm : 0.0);
-      }
-      if (lane == 0) blk->pos = pos;
-      tc_commit();
-      return any;
-    };
-    int nstaged = 0;
+      // records: (chunk-norm suffix after the check point, |c|^2)
+      for (int rr = lane; rr < ROWS; rr += 32) {
+        const int b = rr >> 3, r8 = rr & 7;
+        uint32_t p = bpos[0], v = bval[0];
 #pragma unroll
-    for (int k = 0; k < R - 1; ++k) nstaged += issue(ring + k) ? 1 : 0;
+        for (int bb = 1; bb < SB; ++bb)
+          if (b == bb) {
+            p = bpos[bb];
+            v = bval[bb];
+          }
+        if (uint32_t(r8) < v) {
+          tc_cp16(&st->rec[rr][0], a.SFX + size_t(p + r8) * 2);
+        } else {
+          st->rec[rr][0] = 0.0;
+          st->rec[rr][1] = kPadNorm;
+        }
+      }
+      if (lane < SB) st->pos[lane] = bpos[lane];
+      if (lane == 0) st->nblk = nb;
+      tc_commit();
+      return nb;
+    };
     // adaptive short-circuit: keep checking while at least 1/4 of checks prune
-    bool check = a.short_circuit != 0;
+    bool check = SC && a.short_circuit != 0;
     unsigned n_checks = 0, n_pruned = 0;
+    int pending = 0;  // stages holding at least one block
+#pragma unroll
+    for (int k = 0; k < R - 1; ++k) pending += issue(ring + k) > 0 ? 1 : 0;
 #pragma unroll 1
-    for (int b = 0; b < nstaged; ++b) {
+    for (int st = 0; st < pending; ++st) {
       tc_wait<R - 2>();
       __syncwarp();
-      const TcBlock<NCH>* s = ring + (b % R);
-      const double cn = s->rec[row][3];
-      const uint32_t cpos = s->pos + uint32_t(row);
-#pragma unroll
-      for (int g = 0; g < NGM; ++g) {
-        if (g >= ng) break;
-        double d0 = cn, d1 = cn;
-        bool pruned = false;
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          dmma_8x8x4(d0, d1, s->pts[row][4 * j + col], bq[g][j], d0, d1);
-          if constexpr (NCHECK > 0) {
-            if ((j + 1) % CE == 0 && (j + 1) / CE <= NCHECK && check) {
-              const int c = (j + 1) / CE - 1;
-              const double sf = s->rec[row][c];
-              const bool far = (d0 - sf > qpre[g][c][0]) && (d1 - sf > qpre[g][c][1]);
-              ++n_checks;
-              if (__all_sync(0xffffffffu, far)) {
-                st_skip += NCH - (j + 1);
-                ++n_pruned;
-                pruned = true;
-                break;
-              }
-            }
-          }
-        }
-        ++st_tiles;
-        if (pruned) continue;
-        bool p0 = d0 <= thr[g][0];
-        bool p1 = d1 <= thr[g][1];
-        unsigned m0 = __ballot_sync(0xffffffffu, p0);
-        unsigned m1 = __ballot_sync(0xffffffffu, p1);
-        if ((m0 | m1) == 0) continue;
-        const bool b0 = p0 && (tc_hi_word(d0) - h1[g][0]) <= hw[g][0];
-        const bool b1 = p1 && (tc_hi_word(d1) - h1[g][1]) <= hw[g][1];
-        const uint32_t qa = it.q0 + 8 * g + 2 * col;
-        if (__any_sync(0xffffffffu, b0 || b1)) {
-          const uint2 m = tc_recheck(a.P, DP, a.d, eps_sq, b0, b1, p0, p1, qa, cpos,
-                                     &a.ctr->rechecks);
-          m0 = m.x;
-          m1 = m.y;
-          p0 = (m0 >> lane) & 1u;
-          p1 = (m1 >> lane) & 1u;
-          if ((m0 | m1) == 0) continue;
-        }
-        const int n0 = __popc(m0), n1 = __popc(m1);
-        hb.reserve(n0 + n1, hits, a);
-        if (p0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
-        if (p1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
-        hb.count += n0 + n1;
-        qc[g][0] += p0;
-        qc[g][1] += p1;
+      const TcStage<NCH>* s = ring + (st % R);
+      const int nb = int(s->nblk);
+#pragma unroll 1
+      for (int k = 0; k < nb; k += 2) {
+        st_tiles += uint64_t(min(2, nb - k)) * ng;
+        // (a missing second group / block is padding: its values never pass)
+        tc_step<NCH, SC>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
       }
       if (check && n_checks >= 64 && 4 * n_pruned < n_checks) check = false;
       __syncwarp();
-      nstaged += issue(ring + ((b + R - 1) % R)) ? 1 : 0;
+      pending += issue(ring + ((st + R - 1) % R)) > 0 ? 1 : 0;
     }
     tc_wait<0>();
     // per-query counts (items of one cell may share queries: atomic add)
 #pragma unroll
-    for (int g = 0; g < NGM; ++g) {
+    for (int g = 0; g < NG; ++g) {
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
         unsigned c = qc[g][jj];
@@ -327,10 +395,11 @@ __global__ void __launch_bounds__(kTcThreads, 4) refine_tc_kernel(RefineArgs a) 
 
 int tc_queries_per_item(int d_pad) { return d_pad / 4 <= 8 ? 16 : 8; }
 
-template <int NCH>
+template <int NCH, bool SC>
 static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(TcBlock<NCH>) * kTcWarps * kTcStages + sizeof(uint2) * kTcWarps * kHitBuf;
-  auto kern = refine_tc_kernel<NCH>;
+  const size_t smem =
+      sizeof(TcStage<NCH>) * kTcWarps * kTcStages + sizeof(uint2) * kTcWarps * kHitBuf;
+  auto kern = refine_tc_kernel<NCH, SC>;
   TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcThreads, smem));
@@ -340,23 +409,29 @@ static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
   TJ_CHECK_LAUNCH();
 }
 
+template <int NCH>
+static void launch_tc_sc(const RefineArgs& a, cudaStream_t s) {
+  if (a.short_circuit) launch_tc_t<NCH, true>(a, s);
+  else launch_tc_t<NCH, false>(a, s);
+}
+
 void launch_refine_tc(const RefineArgs& a, cudaStream_t s) {
   switch (a.nchunks) {
-    case 2: return launch_tc_t<2>(a, s);
-    case 3: return launch_tc_t<3>(a, s);
-    case 4: return launch_tc_t<4>(a, s);
-    case 5: return launch_tc_t<5>(a, s);
-    case 6: return launch_tc_t<6>(a, s);
-    case 7: return launch_tc_t<7>(a, s);
-    case 8: return launch_tc_t<8>(a, s);
-    case 9: return launch_tc_t<9>(a, s);
-    case 10: return launch_tc_t<10>(a, s);
-    case 11: return launch_tc_t<11>(a, s);
-    case 12: return launch_tc_t<12>(a, s);
-    case 13: return launch_tc_t<13>(a, s);
-    case 14: return launch_tc_t<14>(a, s);
-    case 15: return launch_tc_t<15>(a, s);
-    case 16: return launch_tc_t<16>(a, s);
+    case 2: return launch_tc_sc<2>(a, s);
+    case 3: return launch_tc_sc<3>(a, s);
+    case 4: return launch_tc_sc<4>(a, s);
+    case 5: return launch_tc_sc<5>(a, s);
+    case 6: return launch_tc_sc<6>(a, s);
+    case 7: return launch_tc_sc<7>(a, s);
+    case 8: return launch_tc_sc<8>(a, s);
+    case 9: return launch_tc_sc<9>(a, s);
+    case 10: return launch_tc_sc<10>(a, s);
+    case 11: return launch_tc_sc<11>(a, s);
+    case 12: return launch_tc_sc<12>(a, s);
+    case 13: return launch_tc_sc<13>(a, s);
+    case 14: return launch_tc_sc<14>(a, s);
+    case 15: return launch_tc_sc<15>(a, s);
+    case 16: return launch_tc_sc<16>(a, s);
     default: break;
   }
   fail(TJ_EINVAL, "DMMA refine is instantiated for 5 <= d <= 64, got d=" + std::to_string(a.d));
