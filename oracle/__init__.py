@@ -49,6 +49,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_sqdist.restype = f64
         L.oracle_sqdist.argtypes = [vp, i64, i32, i64, i64]
         L.oracle_num_threads.restype = i32
+        L.oracle_time_join.restype = i64
+        L.oracle_time_join.argtypes = [vp, i64, i32, i64, i32, f64, vp, i64, i32,
+                                       ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.oracle_rows.restype = i32
         L.oracle_rows.argtypes = [vp, i64, i32, i64, i32, f64, vp, i64, vp, vp, i32]
         _lib = L
@@ -130,6 +133,26 @@ def sqdist(data, i: int, j: int) -> float:
     """Reference direct-form squared distance of points i and j (oracle.py:78-81)."""
     x, d = _coords(data)
     return lib().oracle_sqdist(x.ctypes.data, x.shape[1], d, int(i), int(j))
+
+
+def time_join(data, eps: float, cells=None, k_idx: int | None = None, threads: int = 0):
+    """(grid seconds, refine seconds, pairs) of the reference algorithm on the host cores.
+
+    The grid over all points is built once; only `cells` (indices into the
+    lexicographic cell list; None = all) are refined, in one emitting pass.
+    """
+    x, d = _coords(data)
+    n, ld = x.shape
+    k = min(d, 6) if k_idx is None else int(k_idx)
+    sel = None if cells is None else np.ascontiguousarray(cells, dtype=np.int64)
+    gs, rs = ctypes.c_double(), ctypes.c_double()
+    pairs = lib().oracle_time_join(x.ctypes.data, n, d, ld, k, float(eps),
+                                   None if sel is None else sel.ctypes.data,
+                                   0 if sel is None else len(sel), threads,
+                                   ctypes.byref(gs), ctypes.byref(rs))
+    if pairs < 0:
+        raise RuntimeError("oracle_time_join failed")
+    return gs.value, rs.value, int(pairs)
 
 
 def num_threads() -> int:

@@ -322,6 +322,73 @@ int oracle_rows(const double* x, int64_t n, int d, int64_t ld, int k, double eps
   return 0;
 }
 
+/* CPU-baseline timing (bench.py cpu_baseline / --impl reference): the grid is
+ * built once (timed: *grid_s), then the selected query cells are refined in ONE
+ * pass that emits every pair into per-thread buffers and sorts each row
+ * (timed: *refine_s) -- the reference's per-batch work (join.py:184-204)
+ * without the count pass oracle_self_join needs to size its output.
+ * Returns the number of pairs emitted, < 0 on failure. */
+#include <time.h>
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+int64_t oracle_time_join(const double* x, int64_t n, int d, int64_t ld, int k, double eps,
+                         const int64_t* sel_cells, int64_t n_sel, int threads, double* grid_s,
+                         double* refine_s) {
+  grid_t g;
+  double t0 = now_s();
+  if (k < 1 || k > MAXK || build_grid(x, n, d, ld, k, eps, &g) != 0) return -1;
+  *grid_s = now_s() - t0;
+  const double eps_sq = eps * eps;
+  const int64_t m = sel_cells ? n_sel : g.n_cells;
+  int max_nb = 1;
+  for (int t = 0; t < k; ++t) max_nb *= 3;
+  int64_t total = 0;
+  t0 = now_s();
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel reduction(+ : total)
+#endif
+  {
+    int64_t* nb = (int64_t*)malloc(sizeof(int64_t) * max_nb);
+    size_t cap = 1 << 16, len = 0;
+    uint32_t* buf = (uint32_t*)malloc(sizeof(uint32_t) * cap);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t s = 0; s < m; ++s) {
+      const int64_t ci = sel_cells ? sel_cells[s] : s;
+      const int nn = neighbours(&g, ci, nb);
+      for (int64_t qp = g.cstart[ci]; qp < g.cstart[ci + 1]; ++qp) {
+        const uint32_t q = g.order[qp];
+        const size_t row0 = len;
+        for (int mm = 0; mm < nn; ++mm)
+          for (int64_t cp = g.cstart[nb[mm]]; cp < g.cstart[nb[mm] + 1]; ++cp) {
+            const uint32_t c = g.order[cp];
+            if (direct_le(x, ld, d, q, c, eps_sq)) {
+              if (len == cap) {
+                cap *= 2;
+                buf = (uint32_t*)realloc(buf, sizeof(uint32_t) * cap);
+              }
+              buf[len++] = c;
+            }
+          }
+        qsort(buf + row0, len - row0, sizeof(uint32_t), cmp_u32);
+        total += (int64_t)(len - row0);
+        if (len > (1u << 24)) len = 0; /* rows are consumed; keep the buffer bounded */
+      }
+    }
+    free(buf);
+    free(nb);
+  }
+  *refine_s = now_s() - t0;
+  free_grid(&g);
+  return total;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
