@@ -179,11 +179,10 @@ __device__ __noinline__ void pool_sort(uint32_t* pool, int len) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (mx <= 1) return;
-  if (mx <= 16) pool_sort_n<16>(pool, len);
-  else if (mx <= 32) pool_sort_n<32>(pool, len);
-  else if (mx <= 48) pool_sort_n<48>(pool, len);
+  // three network sizes only: warps of one launch mostly share one network, so
+  // the straight-line code stays resident in the instruction cache
+  if (mx <= 32) pool_sort_n<32>(pool, len);
   else if (mx <= 64) pool_sort_n<64>(pool, len);
-  else if (mx <= 80) pool_sort_n<80>(pool, len);
   else pool_sort_n<96>(pool, len);
 }
 
@@ -360,22 +359,26 @@ __device__ __forceinline__ uint32_t run_position(const uint2* __restrict__ runs,
 
 // Short rows (<= kPoolSlots ids), one per lane, expanded, sorted and placed in
 // one pass.  The lane's mask row (its query group, ~1 KB) is first prefetched
-// into L1 with independent prefetches (one round trip instead of one per 4
-// masks); the lane then walks it and collects its candidate offsets in column
-// `lane` of a transposed shared-memory pool (ascending), maps them to positions
-// by a branch-free binary search in its cell's run table (shared memory,
-// staged once per window for up to kEmitCells cells) and to original ids with
-// 16 independent gathers in flight; the warp sorts the 32 rows in registers
-// (odd-even merge network) and writes them to their places.  Longer rows are
-// listed for long_rows_kernel (warp per row).
+// into L1 with independent prefetches (one round trip instead of one per
+// load).  The lane then walks it four blocks at a time: the four blocks' row
+// bits are packed into one word (bit 4r + u = candidate r of block u), so the
+// divergent hit loop runs once per four blocks; hit offsets go to column `lane`
+// of a transposed shared-memory pool (order is irrelevant: rows are sorted by
+// id at the end).  Offsets map to positions through the cell's run table with a
+// per-block run hint (both staged in shared memory once per window for up to
+// kEmitCells cells), positions to original ids with 16 gathers in flight; the
+// warp sorts the 32 rows in registers (odd-even merge network per lane) and
+// writes them to their places.  Longer rows are listed for long_rows_kernel.
 constexpr int kEmitWarps = 4;
 constexpr int kEmitCells = 8;   // cells of one window whose run tables are staged
 constexpr int kRunTab = 32;     // >= 27 runs (k <= 4) + the list-length sentinel
+constexpr int kBlkTab = 256;    // block -> run hints per staged cell (2048 candidates)
 
 struct EmitSmem {
   uint32_t pool[kPoolSlots * kPoolLd];
-  uint32_t roff[kEmitCells][kRunTab];  // run offsets, padded with 0xffffffff
-  uint32_t rpos[kEmitCells][kRunTab];  // run start positions
+  uint32_t roff[kEmitCells][kRunTab];      // run offsets, padded with 0xffffffff
+  uint32_t rpos[kEmitCells][kRunTab];      // run start positions
+  unsigned char brun[kEmitCells][kBlkTab]; // run holding candidate 8b of block b
 };
 
 __device__ __forceinline__ void prefetch_l1(const void* p) {
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
       mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
       for (int b = 0; b < mr.nblk; b += 4) prefetch_l1(mr.m + b);
     }
-    // run tables of the window's first kEmitCells cells (lanes = runs)
+    // run tables + block hints of the window's first kEmitCells cells
     const int ncw = int(min(__shfl_sync(0xffffffffu, c, 31) + 1, n_cells) - c0);
     __syncwarp();
     for (int ci = 0; ci < min(ncw, kEmitCells); ++ci) {
@@ -421,39 +424,49 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
       sm.rpos[ci][lane] = lane < nr ? runs[rb + lane].x : 0u;
     }
     __syncwarp();
+    for (int ci = 0; ci < min(ncw, kEmitCells); ++ci) {
+      const int nblk = int(min((cell_cand[c0 + ci] + 7) >> 3, int64_t(kBlkTab)));
+      const uint32_t* ro = sm.roff[ci];
+      for (int b = lane; b < nblk; b += 32) {
+        const uint32_t t = 8u * uint32_t(b);
+        int r = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (ro[r + step] <= t) r += step;
+        sm.brun[ci][b] = (unsigned char)r;
+      }
+    }
+    __syncwarp();
     if (pooled) {
-      // 1. candidate offsets, ascending
       uint32_t* col = pool + lane;
+      const int ci = int(c - c0);
+      // 1. candidate offsets (four blocks per packed word)
       int slot = 0;
-      for (int b0 = 0; b0 < mr.nblk; b0 += 8) {
-        unsigned long long v[8];
+      for (int b0 = 0; b0 < mr.nblk; b0 += 4) {
+        unsigned wbits = 0u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b0 + u < mr.nblk ? mr.m[b0 + u] : 0ull;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          unsigned bits = row_bits(v[u], mr.shift);
-          while (bits) {
-            const int r = (__ffs(bits) - 1) >> 2;
-            bits &= bits - 1u;
-            col[slot * kPoolLd] = uint32_t(8 * (b0 + u) + r);
-            ++slot;
-          }
+        for (int u = 0; u < 4; ++u)
+          if (b0 + u < mr.nblk) wbits |= row_bits(mr.m[b0 + u], mr.shift) << u;
+        while (wbits) {
+          const int j = __ffs(wbits) - 1;
+          wbits &= wbits - 1u;
+          col[slot * kPoolLd] = uint32_t(8 * (b0 + (j & 3)) + (j >> 2));
+          ++slot;
         }
       }
-      // 2. offsets -> positions (run table)
-      const int ci = int(c - c0);
-      if (ci < kEmitCells) {
+      // 2. offsets -> positions: the block's run hint, then the (rare) steps to
+      //    later runs when the block straddles a run boundary
+      if (ci < kEmitCells && mr.nblk <= kBlkTab) {
         const uint32_t* ro = sm.roff[ci];
         const uint32_t* rp = sm.rpos[ci];
+        const unsigned char* br = sm.brun[ci];
         for (int i = 0; i < len; ++i) {
           const uint32_t t = col[i * kPoolLd];
-          int r = 0;  // last run with offset <= t (ro[0] == 0; padding is 0xffffffff)
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1)
-            if (ro[r + step] <= t) r += step;
+          int r = br[t >> 3];
+          while (ro[r + 1] <= t) ++r;
           col[i * kPoolLd] = rp[r] + (t - ro[r]);
         }
-      } else {  // more than kEmitCells cells in the window (tiny cells): global search
+      } else {  // many tiny cells in the window, or a very long list: global search
         const int64_t rb = cell_runs[c];
         const int nr = int(cell_runs[c + 1] - rb);
         for (int i = 0; i < len; ++i)
