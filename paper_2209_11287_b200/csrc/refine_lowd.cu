@@ -55,6 +55,8 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+constexpr int kWinLd = 8;  // window buffer row: <= 4 groups x (low, high) mask words
+
 struct LowStage {
   double pts[kStageCands][4];  // candidate coordinates (d <= 3: slot 3 holds |c|^2)
   double2 nrm[kStageCands];    // (|c|^2, |c|^2): the C operand pair (d == 4)
@@ -84,12 +86,12 @@ __device__ __noinline__ uint2 recheck_tile(const double* P, int d, double eps_sq
 
 // U consecutive staged blocks k .. k+U-1 against the NG query groups: all
 // U * NG DMMAs are issued before the first compare, then one DSETP + ballot per
-// value; only steps with a passing value look at the guard band.  Lane
-// (block - window start) keeps the block's masks (sel == block).
+// value; only steps with a passing value look at the guard band.  Lane 0
+// writes the blocks' masks to the warp's window buffer (vector stores).
 template <bool FOLD, int NG, int U>
 __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide<NG>& qs,
-                                            const LowStage* s, int k, int sel, uint32_t q0,
-                                            unsigned (&mk)[NG][2]) {
+                                            const LowStage* s, int k, uint32_t* wbuf,
+                                            uint32_t q0) {
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
   double av[U];
@@ -148,15 +150,20 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
         }
     }
   }
+  // the block's masks into the window buffer (one lane, vector stores)
+  if (lane == 0) {
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (sel == k + u) {
+    for (int u = 0; u < U; ++u) {
+      uint32_t* w = wbuf + (k + u) * kWinLd;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        mk[g][0] = m[u][g][0];
-        mk[g][1] = m[u][g][1];
+      for (int g = 0; g < NG; g += 2) {
+        if (g + 1 < NG)
+          *reinterpret_cast<uint4*>(w + 2 * g) = make_uint4(m[u][g][0], m[u][g][1], m[u][g + 1][0], m[u][g + 1][1]);
+        else
+          *reinterpret_cast<uint2*>(w + 2 * g) = make_uint2(m[u][g][0], m[u][g][1]);
       }
     }
+  }
 }
 
 // All tiles of one work item with NG query groups (compile-time, so the block
@@ -166,8 +173,8 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
 // compared and balloted.
 template <bool FOLD, int NG>
 __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& it, LowStage* ring,
-                                          unsigned long long* mrow, int nblk, uint32_t total,
-                                          uint32_t r_off, uint32_t r_pos, int nr) {
+                                          uint32_t* wbuf, unsigned long long* mrow, int nblk,
+                                          uint32_t total, uint32_t r_off, uint32_t r_pos, int nr) {
   constexpr int R = kLowStages;
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
@@ -234,9 +241,6 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
     cp_async_commit();
   };
 
-  unsigned mk[NG][2];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) mk[g][0] = mk[g][1] = 0u;
 #pragma unroll
   for (int k = 0; k < R - 1; ++k) {
     if (k < nst) issue(k, ring + k);
@@ -248,19 +252,23 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
     __syncwarp();
     const LowStage* s = ring + (st % R);
     const int nb = min(8, nblk - 8 * st);
-    const int sel = lane - ((st & 3) << 3);  // lane keeping block k of this stage: sel == k
+    uint32_t* wb = wbuf + ((st & 3) << 3) * kWinLd;  // this stage's 8 blocks of the window
     // NG <= 2: two blocks per step (2 * NG independent DMMAs in flight); an odd
     // stage end runs one padding block, whose rows never pass
     constexpr int U = NG <= 2 ? 2 : 1;
 #pragma unroll 1
-    for (int k = 0; k < nb; k += U) lowd_blocks<FOLD, NG, U>(a, qs, s, k, sel, it.q0, mk);
+    for (int k = 0; k < nb; k += U) lowd_blocks<FOLD, NG, U>(a, qs, s, k, wb, it.q0);
     // window of 32 blocks complete: lane k stores block (window + k) of each group
     if ((st & 3) == 3 || st + 1 == nst) {
+      __syncwarp();
       const int b = ((st >> 2) << 5) + lane;
       if (b < nblk) {
+        const uint2* w = reinterpret_cast<const uint2*>(wbuf + lane * kWinLd);
 #pragma unroll
-        for (int g = 0; g < NG; ++g)
-          mrow[int64_t(g) * nblk + b] = (static_cast<unsigned long long>(mk[g][1]) << 32) | mk[g][0];
+        for (int g = 0; g < NG; ++g) {
+          const uint2 v = w[g];
+          mrow[int64_t(g) * nblk + b] = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+        }
       }
     }
     __syncwarp();
@@ -275,9 +283,11 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
 template <bool FOLD, int NGMAX>
 __global__ void __launch_bounds__(kLowThreads, NGMAX <= 2 ? 5 : 4) refine_lowd_kernel(RefineArgs a) {
   __shared__ LowStage s_ring[kLowWarps][kLowStages];
+  __shared__ __align__(16) uint32_t s_win[kLowWarps][32 * kWinLd];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   LowStage* ring = s_ring[warp];
+  uint32_t* wbuf = s_win[warp];
   unsigned long long st_tiles = 0, st_refined = 0;
 
   for (;;) {
@@ -305,13 +315,15 @@ __global__ void __launch_bounds__(kLowThreads, NGMAX <= 2 ? 5 : 4) refine_lowd_k
     unsigned long long* mrow = a.masks + a.cell_mbase[it.cell - a.cell_base] +
                                ((int64_t(it.q0) - cs) >> 3) * nblk;
     switch (ng) {
-      case 1: lowd_item<FOLD, 1>(a, it, ring, mrow, nblk, total, r_off, r_pos, nr); break;
-      case 2: lowd_item<FOLD, 2>(a, it, ring, mrow, nblk, total, r_off, r_pos, nr); break;
+      case 1: lowd_item<FOLD, 1>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
+      case 2: lowd_item<FOLD, 2>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
       case 3:
-        if constexpr (NGMAX >= 3) lowd_item<FOLD, 3>(a, it, ring, mrow, nblk, total, r_off, r_pos, nr);
+        if constexpr (NGMAX >= 3)
+          lowd_item<FOLD, 3>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
         break;
       default:
-        if constexpr (NGMAX >= 4) lowd_item<FOLD, 4>(a, it, ring, mrow, nblk, total, r_off, r_pos, nr);
+        if constexpr (NGMAX >= 4)
+          lowd_item<FOLD, 4>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
         break;
     }
   }
