@@ -143,6 +143,11 @@ def dist_setup(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.impl == "reference":
             dist.init_process_group("gloo")
+        elif os.environ.get("TJ_DIST_BACKEND", "nccl") == "gloo":
+            # test hook: several ranks sharing the visible GPU(s) (NCCL refuses that)
+            local = local % max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -155,7 +160,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -185,6 +191,15 @@ def traffic_from_profiles(config: str, kernel: str):
 
 
 # ----------------------------------------------------------------- CPU side
+def host_threads() -> int:
+    """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1;
+    the reference arm and the CPU baseline pass an explicit thread count)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def cpu_reference(ds, eps: float, d: int, info_candidates: int, costs, budget_s: float = 20.0,
                   seed: int = 0, grid_s: float | None = None) -> dict:
     """Reference algorithm (oracle C port of grid.py + the scalar refiner, all host
@@ -194,7 +209,7 @@ def cpu_reference(ds, eps: float, d: int, info_candidates: int, costs, budget_s:
     grid + refine_sample * C / C_sample."""
     import oracle
 
-    threads = oracle.num_threads()
+    threads = host_threads()
     n_cells = len(costs)
     total = int(costs.sum())
     rng = np.random.default_rng(seed)
@@ -241,7 +256,7 @@ def run_reference(args, world, rank):
     ds = generate(GenSpec(dist_name, n, d, seed=0))
     order, cstart, ccoord, cand = oracle.grid(ds, eps, min(d, 6))
     costs = np.diff(cstart) * cand
-    grid_s, _, _ = oracle.time_join(ds, eps, cells=np.zeros(1, np.int64), threads=oracle.num_threads())
+    grid_s, _, _ = oracle.time_join(ds, eps, cells=np.zeros(1, np.int64), threads=host_threads())
     vals = []
     per_step = args.cpu_budget / max(args.steps + args.warmup, 1)
     for i in range(args.warmup + args.steps):
@@ -332,9 +347,15 @@ def run_ours(args, world, rank, local):
     def measure(kernel_cfg, steps, warmup, min_warm_s=1.0):
         with ClockSampler(dev) as clk:
             clk.wait_first()
-            # >= `warmup` steps and >= min_warm_s of load, so the clock sampler sees the GPU busy
+            # >= `warmup` steps and >= min_warm_s of load, so the clock sampler sees the GPU
+            # busy; ranks agree on every extra step (each step holds a collective)
             t_w, done = time.monotonic(), 0
-            while done < warmup or time.monotonic() - t_w < min_warm_s:
+            while True:
+                more = done < warmup or time.monotonic() - t_w < min_warm_s
+                if world > 1:
+                    more = max_over_ranks(1.0 if more else 0.0, world) > 0.5
+                if not more:
+                    break
                 one_step(kernel_cfg)
                 flush.zero_()
                 done += 1
@@ -403,12 +424,14 @@ def run_ours(args, world, rank, local):
         for i in range(args.warmup + args.steps):
             barrier(world)
             t = time.perf_counter()
-            shard_self_join(ds, cfg)
+            _, host_csr, _ = shard_self_join(ds, cfg)
             el = max_over_ranks(time.perf_counter() - t, world)
             if i >= args.warmup:
                 ts.append(el)
         e2e_s = float(np.mean(ts))
         e2e_val = 2.0 * d * C / e2e_s / 1e12
+        if host_csr is not None:
+            d2h = host_csr[0].nbytes + host_csr[1].nbytes
 
     if rank != 0:
         return
@@ -446,7 +469,8 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "seconds": e2e_s,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "self_join(host Dataset, JoinConfig) -> CSR in pinned host memory"
-                       if world == 1 else "distributed.shard_self_join (NCCL bcast, gloo gather)"},
+                       if world == 1 else "distributed.shard_self_join (NCCL bcast, device-side CSR "
+                                          "combine, one D2H on rank 0)"},
         "gpu_launches": launches,
         "guard_rechecks": timings[0]["rechecks"],
         "clocks": clocks,

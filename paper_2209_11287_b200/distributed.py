@@ -5,8 +5,10 @@ with one broadcast (NCCL over NVLink on GPUs, gloo in the CPU tests), every
 rank rebuilds the same deterministic grid, the lexicographic cell list is cut
 into contiguous ranges of equal estimated cost (|cell| * |cand(cell)|, the
 reference estimator join.py:122-124), each rank refines only its query cells
-and emits canonical CSR rows for its own queries, and the rows are gathered to
-the root host.  There is no collective on the refine path itself.
+and emits canonical CSR rows for its own queries, and the rows are combined on
+the devices (count all-reduce + one reduce of the disjoint rows) and copied to
+the root host once.  There is no collective on the refine path itself.
+`gather_csr` is the host-memory (gloo) variant used by the CPU tests.
 """
 
 from __future__ import annotations
@@ -108,11 +110,45 @@ def gather_csr(offsets: np.ndarray, neighbors: np.ndarray, root: int = 0, group=
     return goff, out
 
 
+def gather_csr_device(offsets, neighbors, total: int, root: int = 0, group=None):
+    """Device-side gather of per-rank CSR shards (disjoint non-empty rows) to `root`.
+
+    offsets: device int64[n+1] of this rank's rows (rows it does not own are
+    empty); neighbors: device int32[>= total].  The per-row counts are summed
+    with one all-reduce (NCCL over NVLink on GPUs), every rank places its rows
+    at their global offsets in a full-length buffer and one reduce(SUM) lands
+    the union on `root`'s device (rows are disjoint, so the sum is the union).
+    Returns (offsets, neighbors) device tensors on root, None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    counts = offsets[1:] - offsets[:-1]
+    gcounts = counts.clone()
+    dist.all_reduce(gcounts, op=dist.ReduceOp.SUM, group=group)
+    goff = torch.zeros_like(offsets)
+    torch.cumsum(gcounts, 0, out=goff[1:])
+    m = int(goff[-1].item())
+    full = torch.zeros(max(m, 1), dtype=torch.int32, device=offsets.device)
+    if total > 0:
+        rows = torch.repeat_interleave(torch.arange(len(counts), device=offsets.device), counts)
+        dest = goff[rows] + (torch.arange(total, device=offsets.device) - offsets[rows])
+        full.index_copy_(0, dest, neighbors[:total])
+    if dist.get_backend(group) == "gloo":  # gloo has no GPU reduce; all-reduce instead
+        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.reduce(full, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return (goff, full[:m]) if rank == root else None
+
+
 def shard_self_join(ds: Dataset | None, config, root: int = 0, group=None):
     """Distributed self-join over the current process group (one GPU per rank).
 
-    Rank `root` holds the dataset; all ranks return their local CSR shard and
-    the root additionally returns the gathered global CSR.
+    Rank `root` holds the dataset; the coordinates are broadcast (NCCL over
+    NVLink), every rank refines its cost-balanced cell range, the CSR shards are
+    combined on the device (gather_csr_device) and only `root` copies the
+    result to its host.  Returns (local device CSR, root host CSR or None, job).
     """
     import torch
     import torch.distributed as dist
@@ -121,7 +157,6 @@ def shard_self_join(ds: Dataset | None, config, root: int = 0, group=None):
 
     device = torch.cuda.current_device()
     host, coords, d = broadcast_dataset(ds, root=root, group=group, device=f"cuda:{device}")
-    host_group = _host_group(group)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = coords.shape[0]
     work = host if host is not None else Dataset._wrap(np.empty((n, coords.shape[1])), d)
@@ -130,10 +165,12 @@ def shard_self_join(ds: Dataset | None, config, root: int = 0, group=None):
     costs = job.ctx.cell_costs(info.n_cells)
     lo, hi = balanced_cell_ranges(costs, world)[rank]
     job.refine(cell_range=(lo, hi))
-    job.finalize()
-    off, nbr = job.fetch()
-    merged = gather_csr(off, nbr, root=root, group=host_group)
-    return (off, nbr), merged, job
+    off_d, nbr_d = job.finalize()
+    merged = gather_csr_device(off_d, nbr_d, job.total, root=root, group=group)
+    host_csr = None
+    if merged is not None:
+        host_csr = (merged[0].cpu().numpy(), merged[1].cpu().numpy())
+    return (off_d, nbr_d), host_csr, job
 
 
 _host_groups: dict = {}
