@@ -38,7 +38,7 @@ namespace tj {
 
 constexpr int kLowWarps = 4;
 constexpr int kLowThreads = kLowWarps * kWarp;
-constexpr int kLowStages = 3;  // cp.async ring depth per warp (stages of 8 blocks)
+constexpr int kLowStages = 2;  // cp.async ring depth per warp (stages of 8 blocks)
 constexpr int kStageCands = 64;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -171,11 +171,10 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
 // candidates at a time and every 8-candidate block is multiplied against the
 // NG query fragments back to back (independent DMMAs in flight), then
 // compared and balloted.
-template <bool FOLD, int NG>
+template <bool FOLD, int NG, int R, bool U2ALL>
 __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& it, LowStage* ring,
                                           uint32_t* wbuf, unsigned long long* mrow, int nblk,
                                           uint32_t total, uint32_t r_off, uint32_t r_pos, int nr) {
-  constexpr int R = kLowStages;
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
   const int nq = int(it.nq);
@@ -255,7 +254,7 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
     uint32_t* wb = wbuf + ((st & 3) << 3) * kWinLd;  // this stage's 8 blocks of the window
     // NG <= 2: two blocks per step (2 * NG independent DMMAs in flight); an odd
     // stage end runs one padding block, whose rows never pass
-    constexpr int U = NG <= 2 ? 2 : 1;
+    constexpr int U = (NG <= 2 || U2ALL) ? 2 : 1;
 #pragma unroll 1
     for (int k = 0; k < nb; k += U) lowd_blocks<FOLD, NG, U>(a, qs, s, k, wb, it.q0);
     // window of 32 blocks complete: lane k stores block (window + k) of each group
@@ -280,9 +279,9 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
 
 // NGMAX: largest query-group count of an item (items hold <= 8 * NGMAX queries);
 // NGMAX = 2 keeps the kernel within 102 registers (5 CTAs = 20 warps per SM).
-template <bool FOLD, int NGMAX>
-__global__ void __launch_bounds__(kLowThreads, NGMAX <= 2 ? 5 : 4) refine_lowd_kernel(RefineArgs a) {
-  __shared__ LowStage s_ring[kLowWarps][kLowStages];
+template <bool FOLD, int NGMAX, int R, bool U2ALL, int MINB>
+__global__ void __launch_bounds__(kLowThreads, MINB) refine_lowd_kernel(RefineArgs a) {
+  __shared__ LowStage s_ring[kLowWarps][R];
   __shared__ __align__(16) uint32_t s_win[kLowWarps][32 * kWinLd];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -315,15 +314,15 @@ __global__ void __launch_bounds__(kLowThreads, NGMAX <= 2 ? 5 : 4) refine_lowd_k
     unsigned long long* mrow = a.masks + a.cell_mbase[it.cell - a.cell_base] +
                                ((int64_t(it.q0) - cs) >> 3) * nblk;
     switch (ng) {
-      case 1: lowd_item<FOLD, 1>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
-      case 2: lowd_item<FOLD, 2>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
+      case 1: lowd_item<FOLD, 1, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
+      case 2: lowd_item<FOLD, 2, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
       case 3:
         if constexpr (NGMAX >= 3)
-          lowd_item<FOLD, 3>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
+          lowd_item<FOLD, 3, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
         break;
       default:
         if constexpr (NGMAX >= 4)
-          lowd_item<FOLD, 4>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
+          lowd_item<FOLD, 4, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
         break;
     }
   }
@@ -338,9 +337,9 @@ static int lowd_ngmax(int64_t, int64_t) { return 4; }
 
 int lowd_queries_per_item(int64_t n, int64_t n_cells) { return 8 * lowd_ngmax(n, n_cells); }
 
-template <bool FOLD, int NGMAX>
+template <bool FOLD, int NGMAX, int R, bool U2ALL, int MINB>
 static void launch_lowd_t(const RefineArgs& a, cudaStream_t s) {
-  auto kern = refine_lowd_kernel<FOLD, NGMAX>;
+  auto kern = refine_lowd_kernel<FOLD, NGMAX, R, U2ALL, MINB>;
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLowThreads, 0));
   per_sm = std::max(per_sm, 1);
@@ -349,11 +348,20 @@ static void launch_lowd_t(const RefineArgs& a, cudaStream_t s) {
   TJ_CHECK_LAUNCH();
 }
 
+// Configuration measured best on c2/c4 d<=3 (tools/var_lowd.sh sweep): a
+// 2-stage ring (64 candidates each), two-block steps for NG <= 2, 5 CTAs = 20
+// warps per SM (<= 102 registers).
+template <bool FOLD>
+static void launch_lowd_v(const RefineArgs& a, cudaStream_t s) {
+  launch_lowd_t<FOLD, 4, kLowStages, false, 5>(a, s);
+}
+
 void launch_refine_lowd(const RefineArgs& a, int64_t n, int64_t n_cells, cudaStream_t s) {
   if (a.d_pad != 4) fail(TJ_EINVAL, "low-d DMMA refine needs d <= 4");
-  const bool big = lowd_ngmax(n, n_cells) > 2;
-  if (a.d <= 3) big ? launch_lowd_t<true, 4>(a, s) : launch_lowd_t<true, 2>(a, s);
-  else big ? launch_lowd_t<false, 4>(a, s) : launch_lowd_t<false, 2>(a, s);
+  (void)n;
+  (void)n_cells;
+  if (a.d <= 3) launch_lowd_v<true>(a, s);
+  else launch_lowd_v<false>(a, s);
 }
 
 }  // namespace tj

@@ -1,6 +1,9 @@
 """One join of a synthetic workload, for ncu captures of a single refine launch.
 
-    python tools/profile_join.py <dist> <n> <d> <eps> [tile|scalar] [--no-short-circuit]
+    python tools/profile_join.py <dist> <n> <d> <eps> [tile|scalar] [--no-short-circuit] [--reps=K]
+
+With --reps=K the refine is repeated K times and the median kernel time is
+reported (the first launch of a process runs on cold clocks).
 """
 import sys
 from pathlib import Path
@@ -19,8 +22,12 @@ ds = generate(GenSpec(dist, n, d, seed=0))
 coords = torch.from_numpy(ds.coords).cuda()
 job = DeviceJoin(ds, JoinConfig(epsilon=eps, kernel=kernel, short_circuit=sc, device=0))
 info = job.build(coords)
-job.refine()
-ms = job.ctx.last_refine_ms()
+reps = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--reps=")), "1"))
+times = []
+for _ in range(reps):
+    job.refine()
+    times.append(job.ctx.last_refine_ms())
+ms = sorted(times)[len(times) // 2]
 st = job.ctx.stats()
 C = int(info.candidates)
 print(f"{dist} n={n} d={d} eps={eps} {kernel} sc={sc}: C={C:.4g} pairs={int(job.total)} "
