@@ -37,7 +37,7 @@ namespace tj {
 
 constexpr int kTcWarps = 4;
 constexpr int kTcThreads = kTcWarps * kWarp;
-constexpr int kTcStages = 3;  // stages in the per-warp ring
+
 
 template <int NCH>
 struct TcShape {
@@ -227,11 +227,10 @@ __device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH>&
     }
 }
 
-template <int NCH, bool SC>
-__global__ void __launch_bounds__(kTcThreads) refine_tc_kernel(RefineArgs a) {
+template <int NCH, bool SC, int R, int MINB>
+__global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs a) {
   using S = TcShape<NCH>;
   constexpr int DP = S::DP, NG = S::NG, SB = S::SB, ROWS = S::ROWS, PPR = S::PPR, CH = S::CH;
-  constexpr int R = kTcStages;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -395,11 +394,10 @@ __global__ void __launch_bounds__(kTcThreads) refine_tc_kernel(RefineArgs a) {
 
 int tc_queries_per_item(int d_pad) { return d_pad / 4 <= 8 ? 16 : 8; }
 
-template <int NCH, bool SC>
+template <int NCH, bool SC, int R, int MINB>
 static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
-  const size_t smem =
-      sizeof(TcStage<NCH>) * kTcWarps * kTcStages + sizeof(uint2) * kTcWarps * kHitBuf;
-  auto kern = refine_tc_kernel<NCH, SC>;
+  const size_t smem = sizeof(TcStage<NCH>) * kTcWarps * R + sizeof(uint2) * kTcWarps * kHitBuf;
+  auto kern = refine_tc_kernel<NCH, SC, R, MINB>;
   TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcThreads, smem));
@@ -409,10 +407,19 @@ static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
   TJ_CHECK_LAUNCH();
 }
 
+// Ring depth and CTAs per SM measured on d = 8 / 16 / 32 (ring x occupancy
+// sweep): a 2-stage ring at 4 CTAs (16 warps, <= 128 registers) for NCH <= 4,
+// a 3-stage ring at 3 CTAs for wider rows.
+template <int NCH, bool SC>
+static void launch_tc_v(const RefineArgs& a, cudaStream_t s) {
+  if constexpr (NCH <= 4) launch_tc_t<NCH, SC, 2, 4>(a, s);
+  else launch_tc_t<NCH, SC, 3, 3>(a, s);
+}
+
 template <int NCH>
 static void launch_tc_sc(const RefineArgs& a, cudaStream_t s) {
-  if (a.short_circuit) launch_tc_t<NCH, true>(a, s);
-  else launch_tc_t<NCH, false>(a, s);
+  if (a.short_circuit) launch_tc_v<NCH, true>(a, s);
+  else launch_tc_v<NCH, false>(a, s);
 }
 
 void launch_refine_tc(const RefineArgs& a, cudaStream_t s) {
