@@ -191,6 +191,35 @@ def traffic_from_profiles(config: str, kernel: str):
 
 
 # ----------------------------------------------------------------- CPU side
+def measured_hbm_gbs() -> tuple[float, str]:
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the guide's fallback."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def secondary_rooflines(n: int, d: int, dp: int, timings) -> list:
+    """HBM rooflines of the phases around the refine, from the phase CUDA events.
+
+    index: algorithmic bytes = n * (read d_pad coords + write d_pad cell-ordered
+    coords + ceil(d/4) chunk norms + 8 B norm + 12 B key/id) (SURVEY.md 8(d));
+    output (finalize): 4 B per result pair written + 8 B offsets per point.
+    """
+    peak, src = measured_hbm_gbs()
+    idx_ms = float(np.mean([t["index_ms"] for t in timings]))
+    fin_ms = float(np.mean([t["finalize_ms"] for t in timings]))
+    idx_bytes = n * (8 * dp * 2 + 8 * ((d + 3) // 4) + 8 + 12)
+    out_bytes = 4 * timings[0]["pairs"] + 8 * (n + 1)
+    rows = []
+    for name, b, ms in (("index (grid build, all kernels)", idx_bytes, idx_ms),
+                        ("canonical output (count scan + emit + long rows)", out_bytes, fin_ms)):
+        gbs = b / (ms * 1e-3) / 1e9
+        rows.append({"phase": name, "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                     "frac": gbs / peak, "algorithmic_bytes": b, "ms": ms, "peak_source": src})
+    return rows
+
+
 def host_threads() -> int:
     """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1;
     the reference arm and the CPU baseline pass an explicit thread count)."""
@@ -462,6 +491,7 @@ def run_ours(args, world, rank, local):
                      "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, DFMA {peak_dfma:.2f}) TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
                      "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))",
                      "share_of_step": share},
+        "secondary_rooflines": secondary_rooflines(n, d, dp, timings),
         "tc_vs_core": {args.kernel: {"step_ms": step_ms, "refine_kernel_ms": ref_ms,
                                      "refine_tflops": achieved},
                        other: {"step_ms": o_step, "refine_kernel_ms": o_ref,
