@@ -343,3 +343,41 @@ def test_reference_dataset_object_is_accepted():
     r1 = self_join(Foreign(ds), JoinConfig(epsilon=0.1))
     r2 = self_join(ds.logical.copy(), JoinConfig(epsilon=0.1))
     assert np.array_equal(r1.pairs, r2.pairs)
+
+
+@pytest.mark.parametrize("d", [2, 4])
+def test_batches_on_the_mask_path(d):
+    """Several refine batches into one low-d mask result set (join.py:184-197)."""
+    ds = generate(GenSpec("uniform", 20_000, d, seed=11))
+    eps = 0.02 if d == 2 else 0.12
+    one = self_join(ds, JoinConfig(epsilon=eps))
+    est = int(one.stats.candidates_refined)
+    many = self_join(ds, JoinConfig(epsilon=eps, batch_size=max(est // 7, 1)))
+    assert csr_equal(one.offsets, one.neighbors, many.offsets, many.neighbors)
+    assert_oracle_equal(many, ds, eps)
+
+
+@pytest.mark.parametrize("k_idx", [1, 2, 3])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fewer_indexed_dims(k_idx, kernel):
+    """k_idx < d: longer candidate lists, same pair set (grid.py:79-80)."""
+    ds = generate(GenSpec("uniform", 6000, 4, seed=k_idx))
+    eps = 0.1
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, k_idx=k_idx))
+    assert_oracle_equal(r, ds, eps, k_idx=k_idx)
+
+
+def test_tiny_cells_many_cells_per_window():
+    """Cells of ~1 point: 32-row emit windows span more cells than the staged tables."""
+    ds = generate(GenSpec("uniform", 50_000, 3, seed=6))
+    eps = 0.012
+    r = self_join(ds, JoinConfig(epsilon=eps))
+    assert_oracle_equal(r, ds, eps)
+
+
+def test_long_candidate_lists_low_d():
+    """2-D cells of ~400 points: candidate lists beyond the emit's per-block run hints."""
+    ds = generate(GenSpec("uniform", 200_000, 2, seed=8))
+    eps = 0.045
+    r = self_join(ds, JoinConfig(epsilon=eps))
+    assert_oracle_equal(r, ds, eps)
