@@ -22,8 +22,9 @@
 //  * short-circuit (optional, adaptive): one check after half of the chunks; a
 //    tile stops when every entry's partial distance (acc - candidate suffix +
 //    query prefix) exceeds eps^2 + 2*guard -- safe under rounding, decisions
-//    stay exact.  A warp stops checking for the rest of an item when fewer than
-//    a quarter of its first checks prune;
+//    stay exact.  A warp stops checking when its first 64 checks save fewer
+//    DMMAs than they cost (prune rate * (NCH - CH) < 3/4; re-probed every 16
+//    items) and then runs the plain step;
 //  * exact decisions: guard band as in refine_lowd.cu (values above the band's
 //    lower edge re-decided out of line by the reference direct form);
 //  * emission: hits are sparse at these dimensionalities (|R|/C ~ 1e-3), so
@@ -241,6 +242,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
   HitBuffer hb;
   unsigned long long st_tiles_ref = 0, st_tiles = 0, st_skip = 0;
   const double eps_sq = a.eps_sq;
+  bool sc_check = SC && a.short_circuit != 0;
+  unsigned sc_items = 0, n_checks = 0, n_pruned = 0;
 
   for (;;) {
     unsigned long long idx = 0;
@@ -345,9 +348,13 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
       tc_commit();
       return nb;
     };
-    // adaptive short-circuit: keep checking while at least 1/4 of checks prune
-    bool check = SC && a.short_circuit != 0;
-    unsigned n_checks = 0, n_pruned = 0;
+    // adaptive short-circuit: keep checking while at least 1/4 of checks prune;
+    // the verdict carries over to the warp's next items (re-probed every 16)
+    if (SC && (++sc_items & 15u) == 0) {
+      sc_check = true;
+      n_checks = n_pruned = 0;
+    }
+    bool& check = sc_check;
     int pending = 0;  // stages holding at least one block
 #pragma unroll
     for (int k = 0; k < R - 1; ++k) pending += issue(ring + k) > 0 ? 1 : 0;
@@ -357,13 +364,19 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
       __syncwarp();
       const TcStage<NCH>* s = ring + (st % R);
       const int nb = int(s->nblk);
+      st_tiles += uint64_t(nb) * ng;
+      // (a missing second group / block is padding: its values never pass)
+      if (SC && check) {
 #pragma unroll 1
-      for (int k = 0; k < nb; k += 2) {
-        st_tiles += uint64_t(min(2, nb - k)) * ng;
-        // (a missing second group / block is padding: its values never pass)
-        tc_step<NCH, SC>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
+        for (int k = 0; k < nb; k += 2)
+          tc_step<NCH, SC>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
+        // a check costs ~1.5 DMMA issue slots; a prune saves NCH - CH DMMAs
+        if (n_checks >= 64 && 4 * n_pruned * (NCH - CH) < 3 * n_checks) check = false;
+      } else {  // not checking: the plain step (no live flags, no predicated DMMAs)
+#pragma unroll 1
+        for (int k = 0; k < nb; k += 2)
+          tc_step<NCH, false>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
       }
-      if (check && n_checks >= 64 && 4 * n_pruned < n_checks) check = false;
       __syncwarp();
       pending += issue(ring + ((st + R - 1) % R)) > 0 ? 1 : 0;
     }
