@@ -405,6 +405,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     const int64_t p0 = w << 5, p = p0 + lane;
     const bool valid = p < n;
     const int len = valid ? int(qcount[p]) : 0;
+    // windows of cells another rank / batch refined: nothing to do
+    if (__ballot_sync(0xffffffffu, len > 0) == 0u) continue;
     const uint32_t id = valid ? perm[p] : 0u;
     const int64_t dst = valid ? offsets[id] : 0;
     const int64_t c0 = win_cell[w];
