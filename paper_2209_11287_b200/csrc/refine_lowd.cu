@@ -333,9 +333,7 @@ __global__ void __launch_bounds__(kLowThreads, MINB) refine_lowd_kernel(RefineAr
 
 // Items of <= 32 queries (measured on c2: fewer partial groups and less restaging
 // beat the higher occupancy of 16-query items).
-static int lowd_ngmax(int64_t, int64_t) { return 4; }
-
-int lowd_queries_per_item(int64_t n, int64_t n_cells) { return 8 * lowd_ngmax(n, n_cells); }
+int lowd_queries_per_item(int64_t, int64_t) { return 32; }  // NG <= 4 query groups
 
 template <bool FOLD, int NGMAX, int R, bool U2ALL, int MINB>
 static void launch_lowd_t(const RefineArgs& a, cudaStream_t s) {
