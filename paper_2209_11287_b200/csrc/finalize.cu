@@ -359,10 +359,10 @@ __device__ __forceinline__ uint32_t run_position(const uint2* __restrict__ runs,
 
 // Short rows (<= kPoolSlots ids), one per lane, expanded, sorted and placed in
 // one pass.  The lane's mask row (its query group, ~1 KB) is first prefetched
-// into L1 with independent prefetches (one round trip instead of one per
-// load).  The lane then walks it four blocks at a time: the four blocks' row
-// bits are packed into one word (bit 4r + u = candidate r of block u), so the
-// divergent hit loop runs once per four blocks; hit offsets go to column `lane`
+// into L1 with independent prefetches, then walked 16 masks per batch of
+// independent loads (what the prefetch missed costs one round trip per batch);
+// four blocks' row bits are packed into one word (bit 4r + u = candidate r of
+// block u), so the divergent hit loop runs once per four blocks; hit offsets go to column `lane`
 // of a transposed shared-memory pool (order is irrelevant: rows are sorted by
 // id at the end).  Offsets map to positions through the cell's run table with a
 // per-block run hint (both staged in shared memory once per window for up to
@@ -443,18 +443,23 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     if (pooled) {
       uint32_t* col = pool + lane;
       const int ci = int(c - c0);
-      // 1. candidate offsets (four blocks per packed word)
+      // 1. candidate offsets: 16 masks per batch, four blocks per packed word
       int slot = 0;
-      for (int b0 = 0; b0 < mr.nblk; b0 += 4) {
-        unsigned wbits = 0u;
+      for (int b0 = 0; b0 < mr.nblk; b0 += 16) {
+        unsigned long long mv[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (b0 + u < mr.nblk) wbits |= row_bits(mr.m[b0 + u], mr.shift) << u;
-        while (wbits) {
-          const int j = __ffs(wbits) - 1;
-          wbits &= wbits - 1u;
-          col[slot * kPoolLd] = uint32_t(8 * (b0 + (j & 3)) + (j >> 2));
-          ++slot;
+        for (int u = 0; u < 16; ++u) mv[u] = b0 + u < mr.nblk ? mr.m[b0 + u] : 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          unsigned wbits = 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) wbits |= row_bits(mv[4 * q + u], mr.shift) << u;
+          while (wbits) {
+            const int j = __ffs(wbits) - 1;
+            wbits &= wbits - 1u;
+            col[slot * kPoolLd] = uint32_t(8 * (b0 + 4 * q + (j & 3)) + (j >> 2));
+            ++slot;
+          }
         }
       }
       // 2. offsets -> positions: the block's run hint, then the (rare) steps to
