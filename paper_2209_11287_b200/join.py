@@ -39,7 +39,8 @@ def default_k_idx(d: int) -> int:
 class JoinConfig:
     """Join parameters (join.py:30-46); only epsilon affects which pairs are returned.
 
-    kernel: 'tile' = DMMA tensor-core path, 'scalar' = CUDA-core FP64 path.
+    kernel: 'tile' = DMMA tensor-core path, 'scalar' = CUDA-core FP64 path,
+        'auto' = the faster one for this d from measured throughput (extension).
     batch_size: target estimated pairs per batch (None = one batch).
     k_idx: indexed dimensions, default min(d, 6); the device grid supports <= 8.
     thread_count: accepted for compatibility (host threading has no role here).
@@ -182,8 +183,9 @@ def _validate_config(config: JoinConfig) -> None:
     """join.py:218-226."""
     if not np.isfinite(config.epsilon) or config.epsilon <= 0:
         raise ValidationError(f"epsilon must be positive and finite, got {config.epsilon}")
-    if config.kernel not in ("tile", "scalar"):
-        raise ValidationError(f"kernel must be 'tile' or 'scalar', got {config.kernel!r}")
+    if config.kernel not in ("tile", "scalar", "auto"):
+        raise ValidationError(
+            f"kernel must be 'tile', 'scalar' or 'auto', got {config.kernel!r}")
     if config.batch_size is not None and config.batch_size < 1:
         raise ValidationError(f"batch_size must be >= 1, got {config.batch_size}")
     if config.thread_count < 1:
@@ -198,6 +200,26 @@ def resolve_k_idx(config: JoinConfig, d: int) -> int:
         raise ValidationError(
             f"k_idx must be <= {_native.TJ_MAX_K_IDX} on the device grid, got {k_idx}")
     return k_idx
+
+
+# Refine-kernel throughput measured on one B200 (FP64 TFLOP/s, 2*d flops per
+# candidate pair; profiles/r1e/sweep.jsonl): (d, DMMA tile, CUDA-core).  The
+# DMMA formulation wins at every measured d; above the DMMA instantiation
+# (d > 64) only the CUDA-core kernel exists.
+MEASURED_KERNEL_TFLOPS = ((2, 4.44, 1.39), (4, 9.44, 4.71), (8, 13.17, 6.38), (16, 16.78, 6.36),
+                          (32, 19.09, 5.36))
+DMMA_MAX_DIM = 64
+
+
+def resolve_kernel(kernel: str, d: int) -> str:
+    """'tile' / 'scalar' as given; 'auto' picks the faster measured kernel for d
+    (the nearest measured dimensionality), the CUDA-core one beyond d = 64."""
+    if kernel != "auto":
+        return kernel
+    if d > DMMA_MAX_DIM:
+        return "scalar"
+    nearest = min(MEASURED_KERNEL_TFLOPS, key=lambda row: abs(row[0] - d))
+    return "tile" if nearest[1] >= nearest[2] else "scalar"
 
 
 _pinned: dict = {}
@@ -258,7 +280,9 @@ class DeviceJoin:
         self.k_idx = resolve_k_idx(config, work.d)
         self.ctx = _native.context(device if device is not None else config.device)
         self.device = self.ctx.device
-        self.kernel = _native.TJ_KERNEL_DMMA if config.kernel == "tile" else _native.TJ_KERNEL_CORE
+        self.kernel_name = resolve_kernel(config.kernel, work.d)
+        self.kernel = (_native.TJ_KERNEL_DMMA if self.kernel_name == "tile"
+                       else _native.TJ_KERNEL_CORE)
         self.torch = torch
         self.coords = None
         self.info = None
@@ -332,7 +356,7 @@ class DeviceJoin:
             pairs_emitted=int(st.pairs_emitted),
             guard_rechecks=int(st.guard_rechecks),
         )
-        if self.config.kernel == "tile":
+        if self.kernel_name == "tile":
             n_chunks = self.work.d_padded // 4
             if st.tiles_processed or st.candidates_refined == 0:
                 s.tiles_processed = int(st.tiles_processed)

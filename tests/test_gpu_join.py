@@ -381,3 +381,11 @@ def test_long_candidate_lists_low_d():
     eps = 0.045
     r = self_join(ds, JoinConfig(epsilon=eps))
     assert_oracle_equal(r, ds, eps)
+
+
+def test_auto_kernel_matches():
+    ds = generate(GenSpec("uniform", 3000, 5, seed=12))
+    eps = 0.2
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel="auto"))
+    assert_oracle_equal(r, ds, eps)
+    assert r.stats.tiles_processed > 0  # the DMMA path ran

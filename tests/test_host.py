@@ -139,3 +139,12 @@ def test_library_is_built_for_sm100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_auto_kernel_dispatch():
+    """kernel='auto' picks from measured throughput; DMMA wins at every measured d."""
+    from paper_2209_11287_b200.join import resolve_kernel
+
+    assert resolve_kernel("tile", 3) == "tile" and resolve_kernel("scalar", 3) == "scalar"
+    assert all(resolve_kernel("auto", d) == "tile" for d in (1, 2, 4, 8, 16, 33, 64))
+    assert resolve_kernel("auto", 65) == "scalar"
