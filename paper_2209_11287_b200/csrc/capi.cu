@@ -48,6 +48,7 @@ static void require_grid(tj_ctx* ctx) {
 }
 
 static void zero_results(tj_ctx* ctx, cudaStream_t s) {
+  ctx->ctr_valid = false;
   ctx->counters.ensure(sizeof(DevCounters), s);
   TJ_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(DevCounters), s));
   if (ctx->g.n > 0) {
@@ -59,8 +60,8 @@ static void zero_results(tj_ctx* ctx, cudaStream_t s) {
 // Dense hit-mask layout over all cells (low-d path); depends only on the grid.
 static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
   if (ctx->masks_ready) return;
-  const int64_t total = build_mask_bases(ctx, 0, ctx->g.n_cells, s);
-  ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(total, 1), s);
+  build_mask_bases(ctx, 0, ctx->g.n_cells, s);
+  ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(ctx->g.tiles, 1), s);
   build_window_cells(ctx, s);
   ctx->masks_ready = true;
 }
@@ -261,6 +262,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     if (cell_begin < 0 || cell_end > g.n_cells || cell_begin > cell_end)
       fail(TJ_EINVAL, "cell range out of bounds");
     ctx->have_refine_timing = false;
+    ctx->ctr_valid = false;
     if (cell_begin == cell_end) return;
     // The expanded form needs finite norms; beyond that the exact kernel decides.
     const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
@@ -311,7 +313,8 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;
     // low-d rows are counted from the hit masks (pairs per query + total hits)
-    if (lowd) launch_count_rows(ctx, cell_begin, cell_end, &counters(ctx)->hits, s);
+    if (lowd)
+      launch_count_rows(ctx, cell_begin, cell_end, &counters(ctx)->hits, &counters(ctx)->max_row, s);
   });
 }
 
@@ -334,6 +337,8 @@ int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed) {
     DevCounters c{};
     TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
     TJ_CUDA(cudaStreamSynchronize(s));
+    ctx->ctr = c;
+    ctx->ctr_valid = true;
     *total = int64_t(c.pairs + c.hits);
     const bool over_p = c.pairs > ctx->pair_cap;
     if (overflowed) *overflowed = over_p ? 1 : 0;
@@ -360,15 +365,17 @@ int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream
     require_grid(ctx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
-    DevCounters c{};
-    TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
-    TJ_CUDA(cudaStreamSynchronize(s));
+    DevCounters c = ctx->ctr;  // read by tj_result_count since the last refine
+    if (!ctx->ctr_valid) {
+      TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
+      TJ_CUDA(cudaStreamSynchronize(s));
+    }
     if (c.pairs > ctx->pair_cap)
       fail(TJ_ECAPACITY, "result buffer overflowed; call tj_result_count and re-run the batch");
     if (c.pairs > 0 && c.hits > 0)
       fail(TJ_EINVAL, "one result set mixes the low-d DMMA kernel with another kernel");
     if (c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
-    finalize_csr(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits), s);
+    finalize_csr(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits), int64_t(c.max_row), s);
   });
 }
 

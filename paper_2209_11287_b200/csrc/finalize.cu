@@ -315,11 +315,13 @@ __global__ void __launch_bounds__(256)
                       const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
                       const int64_t* __restrict__ cell_cand, int64_t n_cells,
                       const uint32_t* __restrict__ win_cell, int64_t cb, int64_t ce,
-                      uint32_t* __restrict__ qcount, unsigned long long* hits) {
+                      uint32_t* __restrict__ qcount, unsigned long long* hits,
+                      unsigned long long* max_row) {
   const int lane = lane_id();
   const int64_t pb = cell_start[cb], pe = cell_start[ce];
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   unsigned long long tot = 0;
+  unsigned mx = 0;
   for (int64_t w = (pb >> 5) + (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
        (w << 5) < pe; w += warps) {
     const int64_t p0 = w << 5, p = p0 + lane;
@@ -338,7 +340,10 @@ __global__ void __launch_bounds__(256)
     for (; b < mr.nblk; ++b) cnt += __popc(row_bits(__ldg(mr.m + b), mr.shift));
     qcount[p] = cnt;
     tot += cnt;
+    mx = max(mx, cnt);
   }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0 && mx) atomicMax(max_row, (unsigned long long)mx);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   if (lane == 0 && tot) atomicAdd(hits, tot);
@@ -654,11 +659,11 @@ void build_window_cells(tj_ctx* ctx, cudaStream_t s) {
 }
 
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
-                       cudaStream_t s) {
+                       unsigned long long* max_row, cudaStream_t s) {
   count_rows_kernel<<<kNumSMs * 8, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
-      ctx->win_cell.as<uint32_t>(), cb, ce, ctx->qcount.as<uint32_t>(), hits);
+      ctx->win_cell.as<uint32_t>(), cb, ce, ctx->qcount.as<uint32_t>(), hits, max_row);
   TJ_CHECK_LAUNCH();
 }
 
@@ -724,7 +729,7 @@ static void sort_big_rows(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, uint32_t
 }
 
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
-                  int64_t n_mask_hits, cudaStream_t s) {
+                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s) {
   const int64_t n = ctx->g.n;
   ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
   int64_t* cnt = ctx->tmp64.as<int64_t>();
@@ -799,7 +804,9 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
         pos_off, rows, ctx->perm.as<uint32_t>(), offsets, n, nbr, fill, nbig);
     TJ_CHECK_LAUNCH();
   }
-  sort_big_rows(ctx, offsets, nbr, fill, nbig, s);
+  // low-d rows are at most max_mask_row long (count_rows_kernel): rows the
+  // in-warp sorts cannot take exist only beyond kWarpSortMax
+  if (n_mask_hits == 0 || max_mask_row > kWarpSortMax) sort_big_rows(ctx, offsets, nbr, fill, nbig, s);
 }
 
 }  // namespace tj

@@ -587,14 +587,14 @@ struct MaskCountIn {
   }
 };
 
-int64_t build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
+// (The total over all cells is GridState::tiles, already on the host: no read-back.)
+void build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
   const int64_t n = ce - cb;
-  if (n <= 0) return 0;
+  if (n <= 0) return;
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
   ctx->cell_mbase.ensure(sizeof(int64_t) * (n + 1), s);
   scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb},
                  StoreAt<int64_t>{ctx->cell_mbase.as<int64_t>()}, n, sc, s);
-  return read_scalar<int64_t>(sc.total, s);
 }
 
 int64_t build_work_items(tj_ctx* ctx, int64_t cb, int64_t ce, int qpi, int64_t target,

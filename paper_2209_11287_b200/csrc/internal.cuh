@@ -64,7 +64,8 @@ struct DevCounters {
   unsigned long long rechecks;      // guard-band rechecks
   unsigned long long item_next;     // persistent-kernel work counter
   unsigned long long hits;          // pairs recorded as low-d hit masks
-  unsigned long long pad[2];
+  unsigned long long max_row;       // longest low-d row (count_rows_kernel)
+  unsigned long long pad;
 };
 
 // Low-d output: one 64-bit hit mask per (query group, 8-candidate block) tile,
@@ -130,6 +131,8 @@ struct tj_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool have_refine_timing = false;
   bool masks_ready = false;  // low-d mask layout built for the current grid
+  bool ctr_valid = false;    // `ctr` holds the device counters (no refine since the read)
+  tj::DevCounters ctr{};
 };
 
 namespace tj {
@@ -144,7 +147,7 @@ void build_grid(tj_ctx* ctx, const double* coords, int64_t n, int d, int64_t ld,
 int64_t build_work_items(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, int q_per_item,
                          int64_t slice, cudaStream_t s);
 ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
-int64_t build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
+void build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
 void launch_refine_tc(const RefineArgs& a, cudaStream_t s);  // DMMA, 5 <= d <= 64
@@ -167,7 +170,7 @@ void brute_force_join(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld
                       int64_t* offsets, uint32_t* nbr, int64_t* total, cudaStream_t s);
 void build_window_cells(tj_ctx* ctx, cudaStream_t s);
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
-                       cudaStream_t s);
+                       unsigned long long* max_row, cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
-                  int64_t n_mask_hits, cudaStream_t s);
+                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s);
 }  // namespace tj
