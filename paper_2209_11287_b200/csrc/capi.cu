@@ -279,7 +279,8 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     // lowd: items never split a candidate list (each query row comes from one item)
     const int64_t target = lowd ? (int64_t(1) << 60)
                                 : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
-    ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s);
+    ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s,
+                                    lowd ? &counters(ctx)->n_items : nullptr);
     TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
     RefineArgs a{};
     a.P = ctx->P.as<double>();
@@ -292,6 +293,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.cell_start = ctx->cell_start.as<int64_t>();
     a.items = ctx->items.as<WorkItem>();
     a.n_items = ctx->n_items;
+    a.n_items_dev = lowd ? &counters(ctx)->n_items : nullptr;
     a.ctr = counters(ctx);
     a.pairs = ctx->pairs.as<uint2>();
     a.pair_cap = ctx->pair_cap;

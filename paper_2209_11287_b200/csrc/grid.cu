@@ -597,15 +597,24 @@ void build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
                  StoreAt<int64_t>{ctx->cell_mbase.as<int64_t>()}, n, sc, s);
 }
 
+// Returns the item count.  With total_dev != nullptr (unsliced items, bound =
+// cells + points/qpi) the count stays on the device (*total_dev) and the
+// returned value is only an upper bound: no host round trip.
 int64_t build_work_items(tj_ctx* ctx, int64_t cb, int64_t ce, int qpi, int64_t target,
-                         cudaStream_t s) {
+                         cudaStream_t s, unsigned long long* total_dev) {
   const int64_t n = ce - cb;
   if (n <= 0) return 0;
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
   ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
   ItemCountIn in{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb, qpi, target};
   scan_exclusive(in, StoreAt<int64_t>{ctx->tmp64.as<int64_t>()}, n, sc, s);
-  const int64_t total = read_scalar<int64_t>(sc.total, s);
+  int64_t total;
+  if (total_dev) {
+    total = n + ctx->g.n / qpi + 1;
+    TJ_CUDA(cudaMemcpyAsync(total_dev, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  } else {
+    total = read_scalar<int64_t>(sc.total, s);
+  }
   ctx->items.ensure(sizeof(WorkItem) * std::max<int64_t>(total, 1), s);
   item_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(ctx->cell_start.as<int64_t>(),
                                                     ctx->cell_cand.as<int64_t>(), cb, n, qpi,

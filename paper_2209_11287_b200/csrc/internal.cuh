@@ -65,7 +65,7 @@ struct DevCounters {
   unsigned long long item_next;     // persistent-kernel work counter
   unsigned long long hits;          // pairs recorded as low-d hit masks
   unsigned long long max_row;       // longest low-d row (count_rows_kernel)
-  unsigned long long pad;
+  unsigned long long n_items;       // work items of the current launch (device-side count)
 };
 
 // Low-d output: one 64-bit hit mask per (query group, 8-candidate block) tile,
@@ -83,7 +83,8 @@ struct RefineArgs {
   const int64_t* cell_runs;   // (n_cells+1)
   const int64_t* cell_start;  // (n_cells+1)
   const WorkItem* items;
-  int64_t n_items;
+  int64_t n_items;                       // item count, or an upper bound when n_items_dev is set
+  const unsigned long long* n_items_dev; // exact count on the device (nullptr: n_items is exact)
   DevCounters* ctr;
   uint2* pairs;            // append buffer of (query pos, candidate pos)
   unsigned long long pair_cap;
@@ -145,7 +146,7 @@ int radix_sort_pairs(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, int
 void build_grid(tj_ctx* ctx, const double* coords, int64_t n, int d, int64_t ld, int k,
                 double eps, cudaStream_t s);
 int64_t build_work_items(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, int q_per_item,
-                         int64_t slice, cudaStream_t s);
+                         int64_t slice, cudaStream_t s, unsigned long long* total_dev = nullptr);
 ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
 void build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu

@@ -288,12 +288,13 @@ __global__ void __launch_bounds__(kLowThreads, MINB) refine_lowd_kernel(RefineAr
   LowStage* ring = s_ring[warp];
   uint32_t* wbuf = s_win[warp];
   unsigned long long st_tiles = 0, st_refined = 0;
+  const unsigned long long n_items = a.n_items_dev ? *a.n_items_dev : (unsigned long long)a.n_items;
 
   for (;;) {
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(&a.ctr->item_next, 1ull);
     idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= (unsigned long long)a.n_items) break;
+    if (idx >= n_items) break;
     const WorkItem it = a.items[idx];
     const int ng = (int(it.nq) + 7) >> 3;
     // candidate list = the cell's runs concatenated; lane r holds run r
