@@ -166,6 +166,18 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -309,6 +321,38 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU side
+def weak_local_dataset(dist_name: str, n: int, d: int, eps: float, rank: int, world: int):
+    """Rank `rank`'s part of the weak-scaled workload.
+
+    The global dataset is `world` copies of the configured workload laid side by
+    side along dimension 0 (slab r = the generator with seed r, x0 shifted by r:
+    same density, same epsilon, world x the points).  Rank r owns the query
+    cells whose dimension-0 index covers its slab and holds its slab plus a
+    one-cell halo from each neighbouring slab (the candidates of those cells);
+    no data crosses ranks inside the step.  Returns (local Dataset, own points,
+    (lo, hi) dimension-0 cell indices of the owned cells).
+    """
+    from paper_2209_11287_b200.datasets import Dataset, GenSpec, generate
+
+    def slab(r):
+        x = generate(GenSpec(dist_name, n, d, seed=r)).coords
+        x[:, 0] += r
+        return x
+
+    own = slab(rank)
+    c0 = np.floor(own[:, 0] / eps)
+    lo, hi = int(c0.min()), int(c0.max())
+    parts = [own]
+    if rank > 0:
+        h = slab(rank - 1)
+        parts.append(h[np.floor(h[:, 0] / eps) >= lo - 1])
+    if rank < world - 1:
+        h = slab(rank + 1)
+        parts.append(h[np.floor(h[:, 0] / eps) <= hi + 1])
+    coords = np.ascontiguousarray(np.concatenate(parts))
+    return Dataset._wrap(coords, d), len(own), (lo, hi)
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -320,11 +364,18 @@ def run_ours(args, world, rank, local):
     dist_name, n, d, eps = CONFIGS[args.config]
     dev = local
     torch.cuda.set_device(dev)
-    ds = generate(GenSpec(dist_name, n, d, seed=0)) if rank == 0 else None
+    weak = world > 1 and args.scaling == "weak"
+    if weak:  # every rank holds its own slab + halo; nothing is broadcast
+        ds, n_own, (c_lo, c_hi) = weak_local_dataset(dist_name, n, d, eps, rank, world)
+        n = ds.n
+    else:
+        ds = generate(GenSpec(dist_name, n, d, seed=0)) if rank == 0 else None
     cfg = JoinConfig(epsilon=eps, kernel=args.kernel, short_circuit=not args.no_short_circuit,
                      device=dev)
-    # device-resident input on rank 0; other ranks receive it inside the step
-    coords0 = torch.from_numpy(ds.coords).to(f"cuda:{dev}") if rank == 0 else None
+    # device-resident input on rank 0 (strong: other ranks receive it inside the
+    # step) or on every rank (weak: its own slab + halo)
+    coords0 = torch.from_numpy(ds.coords).to(f"cuda:{dev}") if (rank == 0 or weak) else None
+    weak_range = {}  # owned cell range of the (deterministic) local grid, found once
     dp = 4 * ((d + 3) // 4)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream(dev)
@@ -334,7 +385,7 @@ def run_ours(args, world, rank, local):
 
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
-        if world > 1:
+        if world > 1 and not weak:
             coords = coords0 if rank == 0 else torch.empty((n, dp), dtype=torch.float64,
                                                             device=f"cuda:{dev}")
             dist.broadcast(coords, src=0)
@@ -347,7 +398,15 @@ def run_ours(args, world, rank, local):
         info = job.build(coords)
         ev[2].record(stream)
         cell_range = None
-        if world > 1:
+        if weak:
+            if not weak_range:  # first (warm-up) step: locate the owned cells once
+                cc = job.ctx.export(info, job.k_idx)[2][:, 0]
+                cb = int(np.searchsorted(cc, c_lo, side="left"))
+                ce = int(np.searchsorted(cc, c_hi, side="right"))
+                weak_range["r"] = (cb, ce)
+                weak_range["C"] = int(job.ctx.cell_costs(info.n_cells)[cb:ce].sum())
+            cell_range = weak_range["r"]
+        elif world > 1:
             costs = job.ctx.cell_costs(info.n_cells)
             cell_range = balanced_cell_ranges(costs, world)[rank]
         job.refine(cell_range=cell_range)
@@ -408,6 +467,8 @@ def run_ours(args, world, rank, local):
     timings, clocks, launches = measure(cfg, args.steps, args.warmup)
     step_ms = max_over_ranks(float(np.mean([t["step_ms"] for t in timings])), world)
     C = timings[0]["candidates"]
+    if weak:  # whole-job work: the owned cells of every rank
+        C = int(round(sum_over_ranks(float(weak_range["C"]), world)))
     value = 2.0 * d * C / (step_ms * 1e-3) / 1e12
 
     # TC vs CUDA-core: the other kernel on the same harness
@@ -446,6 +507,24 @@ def run_ours(args, world, rank, local):
         e2e_s = float(np.mean(ts))
         d2h = (n + 1) * 8 + r.total_pairs * 4
         e2e_val = 2.0 * d * C / e2e_s / 1e12
+    elif weak:
+        # per rank: H2D of its slab + halo, join of its owned cells, D2H of its rows
+        ts = []
+        for i in range(args.warmup + args.steps):
+            barrier(world)
+            t = time.perf_counter()
+            job = DeviceJoin(ds, cfg, device=dev)
+            job.build()
+            job.refine(cell_range=weak_range["r"])
+            job.finalize()
+            off_h, nbr_h = job.fetch()
+            el = max_over_ranks(time.perf_counter() - t, world)
+            if i >= args.warmup:
+                ts.append(el)
+        e2e_s = float(np.mean(ts))
+        e2e_val = 2.0 * d * C / e2e_s / 1e12
+        h2d = int(sum_over_ranks(float(ds.coords.nbytes), world))
+        d2h = int(sum_over_ranks(float(off_h.nbytes + nbr_h.nbytes), world))
     else:
         from paper_2209_11287_b200.distributed import shard_self_join
 
@@ -476,13 +555,18 @@ def run_ours(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "self_join_s": step_ms / 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)",
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)"
+                if not weak else "synthetic: rank r = reference generator seed r, dim 0 shifted by r",
         "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps,
                    "kernel": args.kernel, "short_circuit": cfg.short_circuit,
                    "candidate_pairs": C, "result_pairs": timings[0]["pairs"],
                    "n_cells": timings[0]["n_cells"], "l2": "256 MiB write between steps",
-                   "parallelism": f"cells split by estimated cost over {world} rank(s)"},
+                   "parallelism": (f"weak: {world} slabs of the workload side by side along dim 0, "
+                                   "rank r owns slab r's cells + a one-cell halo, no collectives "
+                                   "in the step") if weak else
+                                  f"cells split by estimated cost over {world} rank(s)"},
         "phases_ms": {k: mean(k) for k in ("bcast_ms", "index_ms", "refine_ms", "refine_kernel_ms",
                                            "finalize_ms")},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -520,6 +604,9 @@ def main():
     ap.add_argument("--kernel", choices=("tile", "scalar"), default="tile")
     ap.add_argument("--no-short-circuit", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="N > 1: weak = each rank owns one workload-sized slab (default, the "
+                         "path shards with no collective); strong = one workload split by cost")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of host-core reference work per run (sampled cells)")
     args = ap.parse_args()

@@ -116,3 +116,34 @@ def test_two_rank_shard_self_join_on_gpu(kernel):
     assert np.array_equal(merged[0], full_off)
     assert np.array_equal(np.asarray(merged[1], np.int64), full_nb.astype(np.int64))
     assert all(r[2] > 0 for r in results) and sum(r[2] for r in results) == int(full_off[-1])
+
+
+def test_weak_scaling_partition_is_exact():
+    """bench.py's weak-scaled partition: each rank's slab + one-cell halo holds every
+    candidate of its owned cells, so its rows equal the global join's rows."""
+    import sys
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    from bench import weak_local_dataset
+
+    n, d, eps, world = 4000, 3, 0.06, 3
+    parts = [weak_local_dataset("uniform", n, d, eps, r, world) for r in range(world)]
+    glob = np.concatenate([p[0].coords[: p[1]] for p in parts])  # slabs in rank order
+    g_off, g_nb = oracle.join_csr(glob, eps)
+    for r, (local, n_own, _) in enumerate(parts):
+        l_off, l_nb = oracle.join_csr(local, eps)
+        # local ids: own slab first (global ids r*n .. r*n+n_own), then halo points
+        halo_gid = []
+        if r > 0:
+            lo_slab = parts[r - 1][0].coords[: n]
+            halo_gid.append((r - 1) * n + np.flatnonzero(
+                np.floor(lo_slab[:, 0] / eps) >= parts[r][2][0] - 1))
+        if r < world - 1:
+            hi_slab = parts[r + 1][0].coords[: n]
+            halo_gid.append((r + 1) * n + np.flatnonzero(
+                np.floor(hi_slab[:, 0] / eps) <= parts[r][2][1] + 1))
+        gid = np.concatenate([r * n + np.arange(n_own)] + halo_gid)
+        for i in range(0, n_own, 97):  # own rows, mapped to global ids
+            mine = np.sort(gid[l_nb[l_off[i]:l_off[i + 1]]])
+            want = g_nb[g_off[r * n + i]:g_off[r * n + i + 1]]
+            assert np.array_equal(mine, want.astype(np.int64)), (r, i)
