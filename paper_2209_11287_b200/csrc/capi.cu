@@ -274,7 +274,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     }
     if (lowd) ensure_masks(ctx, s);
     const int qpi = lowd ? lowd_queries_per_item(g.n, g.n_cells)
-                    : dmma ? tc_queries_per_item(g.d_pad)
+                    : dmma ? tc_queries_per_item(g.d_pad, g.n, g.n_cells)
                            : core_queries_per_item(g.d, g.d_pad);
     // lowd: items never split a candidate list (each query row comes from one item)
     const int64_t target = lowd ? (int64_t(1) << 60)
@@ -310,7 +310,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.short_circuit = short_circuit ? 1 : 0;
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
     if (lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
-    else if (dmma) launch_refine_tc(a, s);
+    else if (dmma) launch_refine_tc(a, g.n, g.n_cells, s);
     else launch_refine_core(a, s);
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;

@@ -151,12 +151,13 @@ ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
 void build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
 void launch_refine_core(const RefineArgs& a, cudaStream_t s);
-void launch_refine_tc(const RefineArgs& a, cudaStream_t s);  // DMMA, 5 <= d <= 64
+void launch_refine_tc(const RefineArgs& a, int64_t n, int64_t n_cells,
+                      cudaStream_t s);  // DMMA, 5 <= d <= 64
 void launch_refine_lowd(const RefineArgs& a, int64_t n, int64_t n_cells,
                         cudaStream_t s);  // d <= 4, unsliced items
 int lowd_queries_per_item(int64_t n, int64_t n_cells);
 int core_queries_per_item(int d, int d_pad);
-int tc_queries_per_item(int d_pad);
+int tc_queries_per_item(int d_pad, int64_t n, int64_t n_cells);
 // finalize.cu
 // output.cu / reorder.cu / verify.cu
 void launch_pair_sq_dists(const double* x, int64_t ld, int d, const int64_t* offsets, int64_t n,

@@ -120,9 +120,8 @@ struct BlockCursor {
   }
 };
 
-template <int NCH>
+template <int NCH, int NG>
 struct TcQuery {
-  static constexpr int NG = TcShape<NCH>::NG;
   double bq[NG][NCH];  // -2 * query chunk, B fragments
   double thr[NG][2];   // pass iff D <= thr (upper edge of the guard band)
   double tlo[NG][2];   // D > tlo: inside the band, decided exactly
@@ -131,14 +130,14 @@ struct TcQuery {
 
 // One step: blocks k and k+1 of stage s (the second may be padding) against
 // the NG query groups -- 2*NG accumulator chains advanced chunk by chunk.
-template <int NCH, bool SC>
-__device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH>& qs,
+template <int NCH, int NG, bool SC>
+__device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH, NG>& qs,
                                         const TcStage<NCH>* s, int k, uint32_t q0, bool& check,
                                         unsigned& n_checks, unsigned& n_pruned,
-                                        unsigned long long& st_skip, unsigned (&qc)[TcShape<NCH>::NG][2],
+                                        unsigned long long& st_skip, unsigned (&qc)[NG][2],
                                         HitBuffer& hb, uint2* hits) {
   using S = TcShape<NCH>;
-  constexpr int NG = S::NG, CH = S::CH;
+  constexpr int CH = S::CH;
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
   const unsigned lt = lanemask_lt();
@@ -228,10 +227,12 @@ __device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH>&
     }
 }
 
-template <int NCH, bool SC, int R, int MINB>
+// NG: query groups per item (2 by default; 4 = 32-query items for big cells at
+// NCH <= 2, where sharing each staged block among more groups pays).
+template <int NCH, bool SC, int R, int MINB, int NG>
 __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs a) {
   using S = TcShape<NCH>;
-  constexpr int DP = S::DP, NG = S::NG, SB = S::SB, ROWS = S::ROWS, PPR = S::PPR, CH = S::CH;
+  constexpr int DP = S::DP, SB = S::SB, ROWS = S::ROWS, PPR = S::PPR, CH = S::CH;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
     const int ng = (nq + 7) >> 3;
 
     // ---- query side
-    TcQuery<NCH> qs;
+    TcQuery<NCH, NG> qs;
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
       const int qb = 8 * g + row;
@@ -369,13 +370,13 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
       if (SC && check) {
 #pragma unroll 1
         for (int k = 0; k < nb; k += 2)
-          tc_step<NCH, SC>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
+          tc_step<NCH, NG, SC>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
         // a check costs ~1.5 DMMA issue slots; a prune saves NCH - CH DMMAs
         if (n_checks >= 64 && 4 * n_pruned * (NCH - CH) < 3 * n_checks) check = false;
       } else {  // not checking: the plain step (no live flags, no predicated DMMAs)
 #pragma unroll 1
         for (int k = 0; k < nb; k += 2)
-          tc_step<NCH, false>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
+          tc_step<NCH, NG, false>(a, qs, s, k, it.q0, check, n_checks, n_pruned, st_skip, qc, hb, hits);
       }
       __syncwarp();
       pending += issue(ring + ((st + R - 1) % R)) > 0 ? 1 : 0;
@@ -405,12 +406,21 @@ __global__ void __launch_bounds__(kTcThreads, MINB) refine_tc_kernel(RefineArgs 
   flush_stats(a, st_tiles_ref, st_tiles_ref * NCH - skip_ref, skip_ref, 0);
 }
 
-int tc_queries_per_item(int d_pad) { return d_pad / 4 <= 8 ? 16 : 8; }
+// 32-query items (NG = 4) when the cells are big enough to fill them (NCH <= 2).
+static bool tc_big_items(int nch, int64_t n, int64_t n_cells) {
+  return nch <= 2 && n >= 48 * n_cells;
+}
 
-template <int NCH, bool SC, int R, int MINB>
+int tc_queries_per_item(int d_pad, int64_t n, int64_t n_cells) {
+  const int nch = d_pad / 4;
+  if (tc_big_items(nch, n, n_cells)) return 32;
+  return nch <= 8 ? 16 : 8;
+}
+
+template <int NCH, bool SC, int R, int MINB, int NG>
 static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(TcStage<NCH>) * kTcWarps * R + sizeof(uint2) * kTcWarps * kHitBuf;
-  auto kern = refine_tc_kernel<NCH, SC, R, MINB>;
+  auto kern = refine_tc_kernel<NCH, SC, R, MINB, NG>;
   TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcThreads, smem));
@@ -424,34 +434,39 @@ static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
 // sweep): a 2-stage ring at 4 CTAs (16 warps, <= 128 registers) for NCH <= 4,
 // a 3-stage ring at 3 CTAs for wider rows.
 template <int NCH, bool SC>
-static void launch_tc_v(const RefineArgs& a, cudaStream_t s) {
-  if constexpr (NCH <= 4) launch_tc_t<NCH, SC, 2, 4>(a, s);
-  else launch_tc_t<NCH, SC, 3, 3>(a, s);
+static void launch_tc_v(const RefineArgs& a, cudaStream_t s, bool big) {
+  constexpr int NG = NCH <= 8 ? 2 : 1;
+  if constexpr (NCH <= 2) {
+    if (big) return launch_tc_t<NCH, SC, 2, 3, 4>(a, s);
+  }
+  if constexpr (NCH <= 4) launch_tc_t<NCH, SC, 2, 4, NG>(a, s);
+  else launch_tc_t<NCH, SC, 3, 3, NG>(a, s);
 }
 
 template <int NCH>
-static void launch_tc_sc(const RefineArgs& a, cudaStream_t s) {
-  if (a.short_circuit) launch_tc_v<NCH, true>(a, s);
-  else launch_tc_v<NCH, false>(a, s);
+static void launch_tc_sc(const RefineArgs& a, cudaStream_t s, bool big) {
+  if (a.short_circuit) launch_tc_v<NCH, true>(a, s, big);
+  else launch_tc_v<NCH, false>(a, s, big);
 }
 
-void launch_refine_tc(const RefineArgs& a, cudaStream_t s) {
+void launch_refine_tc(const RefineArgs& a, int64_t n, int64_t n_cells, cudaStream_t s) {
+  const bool big = tc_big_items(a.nchunks, n, n_cells);
   switch (a.nchunks) {
-    case 2: return launch_tc_sc<2>(a, s);
-    case 3: return launch_tc_sc<3>(a, s);
-    case 4: return launch_tc_sc<4>(a, s);
-    case 5: return launch_tc_sc<5>(a, s);
-    case 6: return launch_tc_sc<6>(a, s);
-    case 7: return launch_tc_sc<7>(a, s);
-    case 8: return launch_tc_sc<8>(a, s);
-    case 9: return launch_tc_sc<9>(a, s);
-    case 10: return launch_tc_sc<10>(a, s);
-    case 11: return launch_tc_sc<11>(a, s);
-    case 12: return launch_tc_sc<12>(a, s);
-    case 13: return launch_tc_sc<13>(a, s);
-    case 14: return launch_tc_sc<14>(a, s);
-    case 15: return launch_tc_sc<15>(a, s);
-    case 16: return launch_tc_sc<16>(a, s);
+    case 2: return launch_tc_sc<2>(a, s, big);
+    case 3: return launch_tc_sc<3>(a, s, big);
+    case 4: return launch_tc_sc<4>(a, s, big);
+    case 5: return launch_tc_sc<5>(a, s, big);
+    case 6: return launch_tc_sc<6>(a, s, big);
+    case 7: return launch_tc_sc<7>(a, s, big);
+    case 8: return launch_tc_sc<8>(a, s, big);
+    case 9: return launch_tc_sc<9>(a, s, big);
+    case 10: return launch_tc_sc<10>(a, s, big);
+    case 11: return launch_tc_sc<11>(a, s, big);
+    case 12: return launch_tc_sc<12>(a, s, big);
+    case 13: return launch_tc_sc<13>(a, s, big);
+    case 14: return launch_tc_sc<14>(a, s, big);
+    case 15: return launch_tc_sc<15>(a, s, big);
+    case 16: return launch_tc_sc<16>(a, s, big);
     default: break;
   }
   fail(TJ_EINVAL, "DMMA refine is instantiated for 5 <= d <= 64, got d=" + std::to_string(a.d));

@@ -389,3 +389,12 @@ def test_auto_kernel_matches():
     r = self_join(ds, JoinConfig(epsilon=eps, kernel="auto"))
     assert_oracle_equal(r, ds, eps)
     assert r.stats.tiles_processed > 0  # the DMMA path ran
+
+
+@pytest.mark.parametrize("sc", [True, False])
+def test_big_cells_high_d_32_query_items(sc):
+    """d = 8 with ~64 points per cell: the high-d DMMA kernel's 32-query items."""
+    ds = generate(GenSpec("uniform", 60_000, 8, seed=21))
+    eps = 0.32
+    r = self_join(ds, JoinConfig(epsilon=eps, short_circuit=sc))
+    assert_oracle_equal(r, ds, eps)
