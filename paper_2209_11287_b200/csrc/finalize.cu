@@ -329,13 +329,15 @@ __global__ void __launch_bounds__(256)
     if (p < pb || p >= pe) continue;
     const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
     unsigned cnt = 0;
-    for (int b = 0; b < mr.nblk; b += 16) {  // 16 independent loads per round trip
-      unsigned long long v[16];
+    int b = 0;
+    for (; b + 4 <= mr.nblk; b += 4) {
+      unsigned long long v[4];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = b + u < mr.nblk ? __ldcs(mr.m + b + u) : 0ull;
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(mr.m + b + u);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) cnt += __popc(row_bits(v[u], mr.shift));
+      for (int u = 0; u < 4; ++u) cnt += __popc(row_bits(v[u], mr.shift));
     }
+    for (; b < mr.nblk; ++b) cnt += __popc(row_bits(__ldg(mr.m + b), mr.shift));
     qcount[p] = cnt;
     tot += cnt;
     mx = max(mx, cnt);
