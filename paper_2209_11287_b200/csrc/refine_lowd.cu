@@ -15,17 +15,19 @@
 //    as the reference tiles it (join.py:257-261): blocks straddle run
 //    boundaries, only the list's last block is padded.  Candidates are staged
 //    64 at a time (two per lane, one coalesced 32-byte row each) into a
-//    per-warp cp.async ring; a warp-uniform run cursor maps list offsets to
-//    cell-ordered positions;
+//    2-stage per-warp cp.async ring (5 CTAs = 20 warps per SM: the measured
+//    best ring depth / occupancy); a warp-uniform run cursor maps list offsets
+//    to cell-ordered positions;
 //  * hit test: one DSETP per value against the guard band's upper edge; in a
 //    step with hits a second DSETP against the lower edge finds the values
 //    inside the band, which (rare) are re-decided out of line by the reference
 //    direct form;
-//  * output: the tile's two ballots form one 64-bit hit mask.  Lane k keeps the
-//    masks of block k of the current 32-block window in registers; a window is
-//    flushed with one coalesced 256-byte store per query group.  No atomics, no
-//    ranking, no counting: finalize.cu counts each row from the masks
-//    (count_rows_kernel) and expands them into sorted CSR rows.
+//  * output: the tile's two ballots form one 64-bit hit mask.  One lane writes
+//    each step's masks to the warp's window buffer in shared memory (vector
+//    stores); a 32-block window is flushed with one coalesced 256-byte store per
+//    query group.  No atomics, no ranking, no counting: finalize.cu counts each
+//    row from the masks (count_rows_kernel) and expands them into sorted CSR
+//    rows.
 // Keep the hot loop small: the whole kernel must stay within the instruction
 // cache (rare paths are __noinline__).
 // JoinStats tiles are ceil(nq/8) * ceil(|cand|/8) per item -- exactly the tiles
