@@ -516,8 +516,7 @@ def run_ours(args, world, rank, local):
             job = DeviceJoin(ds, cfg, device=dev)
             job.build()
             job.refine(cell_range=weak_range["r"])
-            job.finalize()
-            off_h, nbr_h = job.fetch()
+            off_h, nbr_h = job.finalize_fetch()
             el = max_over_ranks(time.perf_counter() - t, world)
             if i >= args.warmup:
                 ts.append(el)

@@ -119,6 +119,13 @@ int tj_reserve_results(tj_ctx* ctx, int64_t pairs);
  * reset are non-empty.  Asynchronous. */
 int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream);
 
+/* tj_finalize in two steps, so the caller can copy the offsets to the host
+ * (another stream) while the rows are built: tj_finalize_offsets writes
+ * offsets (device int64[n+1]); tj_finalize_rows then writes the rows using
+ * those offsets.  Asynchronous. */
+int tj_finalize_offsets(tj_ctx* ctx, int64_t* offsets, void* stream);
+int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, void* stream);
+
 /* Counters accumulated since the last tj_reset_results (synchronous). */
 int tj_get_stats(tj_ctx* ctx, tj_stats* out);
 

@@ -54,6 +54,8 @@ SIGNATURES = {
     "tj_reset_results": (_i32, [_vp, _vp]),
     "tj_reserve_results": (_i32, [_vp, _i64]),
     "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
+    "tj_finalize_offsets": (_i32, [_vp, _vp, _vp]),
+    "tj_finalize_rows": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_get_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
     "tj_cell_costs": (_i32, [_vp, _vp]),
     "tj_pair_sq_dists": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp]),
@@ -189,6 +191,16 @@ class Context:
         self._check(self.lib.tj_finalize(self.handle, offsets.data_ptr(),
                                          neighbors.data_ptr() if neighbors is not None else None,
                                          s.cuda_stream))
+
+    def finalize_offsets(self, offsets, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_finalize_offsets(self.handle, offsets.data_ptr(), s.cuda_stream))
+
+    def finalize_rows(self, offsets, neighbors, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_finalize_rows(
+            self.handle, offsets.data_ptr(),
+            neighbors.data_ptr() if neighbors is not None else None, s.cuda_stream))
 
     def stats(self) -> Stats:
         st = Stats()

@@ -361,23 +361,41 @@ int tj_reset_results(tj_ctx* ctx, void* stream) {
   });
 }
 
+static void finalize_phase(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream,
+                           int phase) {
+  require_grid(ctx);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ctx->last_stream = s;
+  DevCounters c = ctx->ctr;  // read by tj_result_count since the last refine
+  if (!ctx->ctr_valid) {
+    TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaStreamSynchronize(s));
+    ctx->ctr = c;
+    ctx->ctr_valid = true;
+  }
+  if (c.pairs > ctx->pair_cap)
+    fail(TJ_ECAPACITY, "result buffer overflowed; call tj_result_count and re-run the batch");
+  if (c.pairs > 0 && c.hits > 0)
+    fail(TJ_EINVAL, "one result set mixes the low-d DMMA kernel with another kernel");
+  if ((phase & 2) && c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
+  finalize_csr(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits), int64_t(c.max_row), s,
+               phase);
+}
+
 int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream) {
   if (!ctx || !offsets) return TJ_EINVAL;
+  return guarded(ctx, [&] { finalize_phase(ctx, offsets, neighbors, stream, 3); });
+}
+
+int tj_finalize_offsets(tj_ctx* ctx, int64_t* offsets, void* stream) {
+  if (!ctx || !offsets) return TJ_EINVAL;
+  return guarded(ctx, [&] { finalize_phase(ctx, offsets, nullptr, stream, 1); });
+}
+
+int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, void* stream) {
+  if (!ctx || !offsets) return TJ_EINVAL;
   return guarded(ctx, [&] {
-    require_grid(ctx);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    ctx->last_stream = s;
-    DevCounters c = ctx->ctr;  // read by tj_result_count since the last refine
-    if (!ctx->ctr_valid) {
-      TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
-      TJ_CUDA(cudaStreamSynchronize(s));
-    }
-    if (c.pairs > ctx->pair_cap)
-      fail(TJ_ECAPACITY, "result buffer overflowed; call tj_result_count and re-run the batch");
-    if (c.pairs > 0 && c.hits > 0)
-      fail(TJ_EINVAL, "one result set mixes the low-d DMMA kernel with another kernel");
-    if (c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
-    finalize_csr(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits), int64_t(c.max_row), s);
+    finalize_phase(ctx, const_cast<int64_t*>(offsets), neighbors, stream, 2);
   });
 }
 

@@ -728,18 +728,23 @@ static void sort_big_rows(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, uint32_t
   hb.release(s);
 }
 
+// phase 1: row offsets by original id; phase 2: the rows (needs phase 1's
+// offsets); 3: both.  Splitting lets a caller copy the offsets to the host
+// while the rows are being built.
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
-                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s) {
+                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s, int phase) {
   const int64_t n = ctx->g.n;
-  ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
-  int64_t* cnt = ctx->tmp64.as<int64_t>();
-  counts_to_orig_kernel<<<blocks_for(n, 256), 256, 0, s>>>(ctx->qcount.as<uint32_t>(),
-                                                          ctx->perm.as<uint32_t>(), n, cnt);
-  TJ_CHECK_LAUNCH();
   ScanScratch sc = scan_scratch(ctx, n, s);
-  scan_exclusive(LoadAt<int64_t>{cnt}, StoreAt<int64_t>{offsets}, n, sc, s);
-  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  if (n_pairs == 0 && n_mask_hits == 0) return;
+  if (phase & 1) {
+    ctx->tmp64.ensure(sizeof(int64_t) * (n + 1), s);
+    int64_t* cnt = ctx->tmp64.as<int64_t>();
+    counts_to_orig_kernel<<<blocks_for(n, 256), 256, 0, s>>>(ctx->qcount.as<uint32_t>(),
+                                                            ctx->perm.as<uint32_t>(), n, cnt);
+    TJ_CHECK_LAUNCH();
+    scan_exclusive(LoadAt<int64_t>{cnt}, StoreAt<int64_t>{offsets}, n, sc, s);
+    TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  }
+  if (!(phase & 2) || (n_pairs == 0 && n_mask_hits == 0)) return;
 
   // `fill` doubles as the list of rows too long for the in-register sorts
   ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);

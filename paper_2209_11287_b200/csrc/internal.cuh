@@ -174,5 +174,5 @@ void build_window_cells(tj_ctx* ctx, cudaStream_t s);
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
                        unsigned long long* max_row, cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
-                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s);
+                  int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s, int phase = 3);
 }  // namespace tj

@@ -349,6 +349,30 @@ class DeviceJoin:
         torch.cuda.current_stream(self.device).synchronize()
         return off.numpy(), nbr.numpy()
 
+    def finalize_fetch(self):
+        """finalize() + fetch() with the offsets' D2H (side stream) overlapping the
+        row kernels; returns numpy (offsets, neighbors)."""
+        torch = self.torch
+        n = self.work.n
+        dev = f"cuda:{self.device}"
+        main = torch.cuda.current_stream(self.device)
+        self.offsets_d = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.neighbors_d = torch.empty(max(self.total, 1), dtype=torch.int32, device=dev)
+        off = torch.empty((n + 1,), dtype=torch.int64, pin_memory=True)
+        nbr = torch.empty((self.total,), dtype=torch.int32, pin_memory=True)
+        self.ctx.finalize_offsets(self.offsets_d)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        cs = self._copy_stream
+        cs.wait_stream(main)
+        with torch.cuda.stream(cs):
+            off.copy_(self.offsets_d, non_blocking=True)
+        self.ctx.finalize_rows(self.offsets_d, self.neighbors_d)
+        nbr.copy_(self.neighbors_d[: self.total], non_blocking=True)
+        main.synchronize()
+        cs.synchronize()
+        return off.numpy(), nbr.numpy()
+
     def stats(self) -> JoinStats:
         st = self.ctx.stats()
         s = JoinStats(
@@ -409,8 +433,7 @@ def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) 
     job.build(coords)
     t_indexed = time.perf_counter()
     total = job.refine(max_result_pairs=max_result_pairs)
-    job.finalize()
-    offsets, neighbors = job.fetch()
+    offsets, neighbors = job.finalize_fetch()
     t_end = time.perf_counter()
     stats = job.stats()
     stats.pairs_emitted = total

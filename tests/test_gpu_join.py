@@ -398,3 +398,21 @@ def test_big_cells_high_d_32_query_items(sc):
     eps = 0.32
     r = self_join(ds, JoinConfig(epsilon=eps, short_circuit=sc))
     assert_oracle_equal(r, ds, eps)
+
+
+@pytest.mark.parametrize("d,kernel", [(3, "tile"), (8, "tile"), (3, "scalar")])
+def test_split_finalize_matches_one_call(d, kernel):
+    """tj_finalize_offsets + tj_finalize_rows (what self_join uses) == tj_finalize."""
+    from paper_2209_11287_b200.join import DeviceJoin
+
+    ds = generate(GenSpec("uniform", 8000, d, seed=4))
+    eps = 0.08 if d == 3 else 0.5
+    job = DeviceJoin(ds, JoinConfig(epsilon=eps, kernel=kernel), device=0)
+    job.build()
+    job.refine()
+    off_a, nbr_a = job.finalize_fetch()
+    job.finalize()
+    off_b, nbr_b = job.fetch()
+    assert np.array_equal(off_a, off_b) and np.array_equal(nbr_a, nbr_b)
+    off, nb = oracle.join_csr(ds, eps)
+    assert csr_equal(off_a, nbr_a, off, nb)
