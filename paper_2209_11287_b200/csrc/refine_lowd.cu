@@ -19,8 +19,8 @@
 //    best ring depth / occupancy); a warp-uniform run cursor maps list offsets
 //    to cell-ordered positions;
 //  * hit test: one DSETP per value against the guard band's upper edge; in a
-//    step with hits a second DSETP against the lower edge finds the values
-//    inside the band, which (rare) are re-decided out of line by the reference
+//    step with hits a second DSETP + ballot against the lower edge, masked with
+//    the first ballot, finds the values inside the band, which (rare) are re-decided out of line by the reference
 //    direct form;
 //  * output: the tile's two ballots form one 64-bit hit mask.  One lane writes
 //    each step's masks to the warp's window buffer in shared memory (vector
@@ -110,7 +110,6 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
     for (int g = 0; g < NG; ++g)
       dmma_8x8x4(dv[u][g][0], dv[u][g][1], av[u], qs.bq[g], FOLD ? qs.cq[g][0] : cv[u].x,
                  FOLD ? qs.cq[g][1] : cv[u].y);
-  bool pv[U][NG][2];
   unsigned m[U][NG][2];
   unsigned any = 0u;
 #pragma unroll
@@ -119,33 +118,34 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
     for (int g = 0; g < NG; ++g)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        pv[u][g][j] = dv[u][g][j] <= qs.thr[g][j];
-        m[u][g][j] = __ballot_sync(0xffffffffu, pv[u][g][j]);
+        m[u][g][j] = __ballot_sync(0xffffffffu, dv[u][g][j] <= qs.thr[g][j]);
         any |= m[u][g][j];
       }
   if (any) {
-    // passing values above the band's lower edge are decided exactly (one more
-    // DSETP each: measured cheaper than integer screening of the high word)
-    bool bv[U][NG][2];
-    bool band = false;
+    // passing values above the band's lower edge are decided exactly: one more
+    // DSETP per value, balloted and masked with the pass ballot (keeping the
+    // pass predicates alive instead makes ptxas recompute them: 3 DSETP/value)
+    unsigned bm[U][NG][2];
+    unsigned band = 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int g = 0; g < NG; ++g)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          bv[u][g][j] = pv[u][g][j] && dv[u][g][j] > qs.tlo[g][j];
-          band |= bv[u][g][j];
+          bm[u][g][j] = __ballot_sync(0xffffffffu, dv[u][g][j] > qs.tlo[g][j]) & m[u][g][j];
+          band |= bm[u][g][j];
         }
-    if (__any_sync(0xffffffffu, band)) {
+    if (band) {  // warp-uniform
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-          if (__any_sync(0xffffffffu, bv[u][g][0] || bv[u][g][1])) {
-            const uint2 mm = recheck_tile(a.P, a.d, a.eps_sq, bv[u][g][0], bv[u][g][1],
-                                          m[u][g][0], m[u][g][1], q0 + 8 * g + 2 * col,
-                                          s->pos[8 * (k + u) + row], &a.ctr->rechecks);
+          if (bm[u][g][0] | bm[u][g][1]) {
+            const uint2 mm = recheck_tile(a.P, a.d, a.eps_sq, (bm[u][g][0] >> lane) & 1u,
+                                          (bm[u][g][1] >> lane) & 1u, m[u][g][0], m[u][g][1],
+                                          q0 + 8 * g + 2 * col, s->pos[8 * (k + u) + row],
+                                          &a.ctr->rechecks);
             m[u][g][0] = mm.x;
             m[u][g][1] = mm.y;
           }
