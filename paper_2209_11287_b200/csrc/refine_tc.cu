@@ -194,83 +194,49 @@ __device__ __forceinline__ void tc_step(const RefineArgs& a, const TcQuery<NCH, 
       }
     }
   }
-  if constexpr (NG == 4) {
-    // 32-query items (measured: c4 d = 8 238 -> 218 ms): compare + ballot every
-    // tile, one branch for the whole step (hits are rare); pruned tiles hold
-    // partial sums and are masked out.  The 16-query variants keep one branch
-    // per tile (c3 618 -> 628 ms, and c4 d = 16 7.6 -> 8.2 s from spills).
-    unsigned mm[2][NG][2];
-    unsigned any = 0u;
+  // epilogue: one branch for the step on the OR of the compare ballots (not
+  // kept: registers; hits are rare); steps with a hit recompute them per tile.
+  // Pruned tiles hold partial sums and are masked out.
+  unsigned any = 0u;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const unsigned lv = live[u][g] ? 0xffffffffu : 0u;
-        mm[u][g][0] = __ballot_sync(0xffffffffu, acc[u][g][0] <= qs.thr[g][0]) & lv;
-        mm[u][g][1] = __ballot_sync(0xffffffffu, acc[u][g][1] <= qs.thr[g][1]) & lv;
-        any |= mm[u][g][0] | mm[u][g][1];
-      }
-    if (any == 0u) return;
+    for (int g = 0; g < NG; ++g) {
+      const unsigned lv = live[u][g] ? 0xffffffffu : 0u;
+      any |= (__ballot_sync(0xffffffffu, acc[u][g][0] <= qs.thr[g][0]) |
+              __ballot_sync(0xffffffffu, acc[u][g][1] <= qs.thr[g][1])) & lv;
+    }
+  if (any == 0u) return;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        unsigned m0 = mm[u][g][0], m1 = mm[u][g][1];
+    for (int g = 0; g < NG; ++g) {
+      if (!live[u][g]) continue;
+      const bool p0 = acc[u][g][0] <= qs.thr[g][0];
+      const bool p1 = acc[u][g][1] <= qs.thr[g][1];
+      unsigned m0 = __ballot_sync(0xffffffffu, p0);
+      unsigned m1 = __ballot_sync(0xffffffffu, p1);
+      if ((m0 | m1) == 0) continue;
+      const uint32_t cpos = s->pos[k + u] + uint32_t(row);
+      const uint32_t qa = q0 + 8 * g + 2 * col;
+      const bool b0 = p0 && acc[u][g][0] > qs.tlo[g][0];
+      const bool b1 = p1 && acc[u][g][1] > qs.tlo[g][1];
+      if (__any_sync(0xffffffffu, b0 || b1)) {
+        const uint2 m = tc_recheck(a.P, 4 * NCH, a.d, a.eps_sq, b0, b1, m0, m1, qa, cpos,
+                                   &a.ctr->rechecks);
+        m0 = m.x;
+        m1 = m.y;
         if ((m0 | m1) == 0) continue;
-        const bool p0 = (m0 >> lane) & 1u, p1 = (m1 >> lane) & 1u;
-        const uint32_t cpos = s->pos[k + u] + uint32_t(row);
-        const uint32_t qa = q0 + 8 * g + 2 * col;
-        const bool b0 = p0 && acc[u][g][0] > qs.tlo[g][0];
-        const bool b1 = p1 && acc[u][g][1] > qs.tlo[g][1];
-        if (__any_sync(0xffffffffu, b0 || b1)) {
-          const uint2 m = tc_recheck(a.P, 4 * NCH, a.d, a.eps_sq, b0, b1, m0, m1, qa, cpos,
-                                     &a.ctr->rechecks);
-          m0 = m.x;
-          m1 = m.y;
-          if ((m0 | m1) == 0) continue;
-        }
-        const bool h0 = (m0 >> lane) & 1u, h1 = (m1 >> lane) & 1u;
-        const int n0 = __popc(m0), n1 = __popc(m1);
-        hb.reserve(n0 + n1, hits, a);
-        if (h0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
-        if (h1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
-        hb.count += n0 + n1;
-        qc[g][0] += h0;
-        qc[g][1] += h1;
       }
-  } else {
-    // epilogue: compare + ballot; hits are rare
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        if (!live[u][g]) continue;
-        const bool p0 = acc[u][g][0] <= qs.thr[g][0];
-        const bool p1 = acc[u][g][1] <= qs.thr[g][1];
-        unsigned m0 = __ballot_sync(0xffffffffu, p0);
-        unsigned m1 = __ballot_sync(0xffffffffu, p1);
-        if ((m0 | m1) == 0) continue;
-        const uint32_t cpos = s->pos[k + u] + uint32_t(row);
-        const uint32_t qa = q0 + 8 * g + 2 * col;
-        const bool b0 = p0 && acc[u][g][0] > qs.tlo[g][0];
-        const bool b1 = p1 && acc[u][g][1] > qs.tlo[g][1];
-        if (__any_sync(0xffffffffu, b0 || b1)) {
-          const uint2 m = tc_recheck(a.P, 4 * NCH, a.d, a.eps_sq, b0, b1, m0, m1, qa, cpos,
-                                     &a.ctr->rechecks);
-          m0 = m.x;
-          m1 = m.y;
-          if ((m0 | m1) == 0) continue;
-        }
-        const bool h0 = (m0 >> lane) & 1u, h1 = (m1 >> lane) & 1u;
-        const int n0 = __popc(m0), n1 = __popc(m1);
-        hb.reserve(n0 + n1, hits, a);
-        if (h0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
-        if (h1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
-        hb.count += n0 + n1;
-        qc[g][0] += h0;
-        qc[g][1] += h1;
-      }
-  }
+      const bool h0 = (m0 >> lane) & 1u, h1 = (m1 >> lane) & 1u;
+      const int n0 = __popc(m0), n1 = __popc(m1);
+      hb.reserve(n0 + n1, hits, a);
+      if (h0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
+      if (h1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
+      hb.count += n0 + n1;
+      qc[g][0] += h0;
+      qc[g][1] += h1;
+    }
 }
 
 // NG: query groups per item (2 by default; 4 = 32-query items for big cells at
