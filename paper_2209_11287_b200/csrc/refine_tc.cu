@@ -27,8 +27,9 @@
 //    items) and then runs the plain step;
 //  * exact decisions: guard band as in refine_lowd.cu (values above the band's
 //    lower edge re-decided out of line by the reference direct form);
-//  * emission: hits are sparse at these dimensionalities (|R|/C ~ 1e-3), so
-//    pairs go through a per-warp shared-memory buffer flushed with one
+//  * emission: hits are sparse at these dimensionalities (|R|/C ~ 1e-3), so a
+//    step branches once on the OR of all its compare ballots and only steps
+//    with a hit look at tiles one by one; pairs go through a per-warp shared-memory buffer flushed with one
 //    atomicAdd per 256 pairs; per-query counts accumulate in registers and are
 //    added once per item (items of a big cell share queries).
 #include "internal.cuh"
