@@ -45,7 +45,6 @@ template <int NCH>
 struct TcShape {
   static constexpr int DP = 4 * NCH;
   static constexpr int STRIDE = (DP % 8 == 0) ? DP + 4 : DP;  // conflict-free fragment rows
-  static constexpr int NG = NCH <= 8 ? 2 : 1;                  // query groups per item
   static constexpr int SB = NCH <= 4 ? 4 : 2;                  // blocks per stage (even)
   static constexpr int ROWS = 8 * SB;
   static constexpr int PPR = DP / 2;                           // 16-byte pieces per row
@@ -427,7 +426,7 @@ static bool tc_big_items(int nch, int64_t n, int64_t n_cells) {
 int tc_queries_per_item(int d_pad, int64_t n, int64_t n_cells) {
   const int nch = d_pad / 4;
   if (tc_big_items(nch, n, n_cells)) return 32;
-  return nch <= 8 ? 16 : 8;
+  return 16;
 }
 
 template <int NCH, bool SC, int R, int MINB, int NG>
@@ -445,15 +444,17 @@ static void launch_tc_t(const RefineArgs& a, cudaStream_t s) {
 
 // Ring depth and CTAs per SM measured on d = 8 / 16 / 32 (ring x occupancy
 // sweep): a 2-stage ring at 4 CTAs (16 warps, <= 128 registers) for NCH <= 4,
-// a 3-stage ring at 3 CTAs for wider rows.
+// a 3-stage ring at 3 CTAs up to NCH = 8, and above that a 2-stage ring at 2
+// CTAs so two query groups' fragments fit in registers (d = 64: one group per
+// item, 50.6 s -> two groups, 27.9 s).
 template <int NCH, bool SC>
 static void launch_tc_v(const RefineArgs& a, cudaStream_t s, bool big) {
-  constexpr int NG = NCH <= 8 ? 2 : 1;
   if constexpr (NCH <= 2) {
     if (big) return launch_tc_t<NCH, SC, 2, 3, 4>(a, s);
   }
-  if constexpr (NCH <= 4) launch_tc_t<NCH, SC, 2, 4, NG>(a, s);
-  else launch_tc_t<NCH, SC, 3, 3, NG>(a, s);
+  if constexpr (NCH <= 4) launch_tc_t<NCH, SC, 2, 4, 2>(a, s);
+  else if constexpr (NCH <= 8) launch_tc_t<NCH, SC, 3, 3, 2>(a, s);
+  else launch_tc_t<NCH, SC, 2, 2, 2>(a, s);
 }
 
 template <int NCH>
