@@ -151,6 +151,13 @@ int tj_pair_sq_dists(tj_ctx* ctx, const double* coords, int64_t ld, int32_t d,
 int tj_write_pairs(const char* path, const int64_t* offsets, int64_t n,
                    const uint32_t* neighbors, const double* sq, int32_t threads);
 
+/* JoinResult.pairs (join.py:80-91): expand the CSR into (query id, neighbour id)
+ * int64 rows, out[2e] = row, out[2e+1] = neighbors[e].  Host arrays (offsets
+ * int64[n+1], neighbors uint32[offsets[n]], out int64[2*offsets[n]]); `threads`
+ * host threads write disjoint row ranges.  Synchronous. */
+int tj_expand_pairs(const int64_t* offsets, int64_t n, const uint32_t* neighbors, int64_t* out,
+                    int32_t threads);
+
 /* Per-column mean and variance of coords (device, n rows, stride ld, first d
  * columns) into host arrays mean[d], var[d] (synchronous).  Feeds the variance
  * dimension reordering (datasets.reorder_dims_by_variance, datasets.py:113-123);

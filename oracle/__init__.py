@@ -54,6 +54,10 @@ def lib() -> ctypes.CDLL:
                                        ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.oracle_rows.restype = i32
         L.oracle_rows.argtypes = [vp, i64, i32, i64, i32, f64, vp, i64, vp, vp, i32]
+        L.oracle_digest.restype = i32
+        L.oracle_digest.argtypes = [vp, i64, i32, i64, i32, f64, i32, vp]
+        L.oracle_digest_keys.restype = None
+        L.oracle_digest_keys.argtypes = [vp, i64, vp]
         _lib = L
     return _lib
 
@@ -153,6 +157,26 @@ def time_join(data, eps: float, cells=None, k_idx: int | None = None, threads: i
     if pairs < 0:
         raise RuntimeError("oracle_time_join failed")
     return gs.value, rs.value, int(pairs)
+
+
+def digest(data, eps: float, k_idx: int | None = None, threads: int = 0) -> dict:
+    """Order-independent digest of the full reference pair set (direct_join.c
+    oracle_digest): {"pairs", "s1", "s2", "max_row"}; no output is materialised."""
+    x, d = _coords(data)
+    n, ld = x.shape
+    k = min(d, 6) if k_idx is None else int(k_idx)
+    out = np.zeros(4, dtype=np.uint64)
+    if lib().oracle_digest(x.ctypes.data, n, d, ld, k, float(eps), threads, out.ctypes.data) != 0:
+        raise RuntimeError("oracle_digest failed")
+    return {"pairs": int(out[0]), "s1": int(out[1]), "s2": int(out[2]), "max_row": int(out[3])}
+
+
+def digest_keys(keys) -> dict:
+    """The same digest over explicit keys (q << 32 | c), uint64."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    out = np.zeros(3, dtype=np.uint64)
+    lib().oracle_digest_keys(k.ctypes.data, len(k), out.ctypes.data)
+    return {"pairs": int(out[0]), "s1": int(out[1]), "s2": int(out[2])}
 
 
 def num_threads() -> int:

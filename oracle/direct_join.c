@@ -396,3 +396,99 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ---- full-set digest (parity of the large configs without materialising 10+ GB) ----
+ * An order-independent digest of the pair set R = {(q, c)}: with
+ * key = (uint64)q << 32 | c, s1 = sum splitmix64(key), s2 = sum splitmix64(key + K2)
+ * (mod 2^64), plus |R|.  tests/test_gpu_parity.py computes the same digest from the
+ * device CSR (tests/digest.py; the two are pinned against each other on CPU).
+ * The direct form is the reference's (join.py:310-318); the running sum stops once
+ * it exceeds eps^2 -- exact, because fl(acc + t) >= acc for t >= 0, so a partial sum
+ * above eps^2 stays above it. */
+static inline uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+#define DIGEST_K2 0x632be59bd9b4e019ull
+
+static inline int direct_le_exit(const double* a, const double* b, int d, double eps_sq) {
+  double acc = 0.0;
+  int t = 0;
+  for (; t + 4 <= d; t += 4) {
+    double d0 = a[t] - b[t], d1 = a[t + 1] - b[t + 1], d2 = a[t + 2] - b[t + 2],
+           d3 = a[t + 3] - b[t + 3];
+    acc = acc + d0 * d0;
+    acc = acc + d1 * d1;
+    acc = acc + d2 * d2;
+    acc = acc + d3 * d3;
+    if (acc > eps_sq) return 0;
+  }
+  for (; t < d; ++t) {
+    double df = a[t] - b[t];
+    acc = acc + df * df;
+  }
+  return acc <= eps_sq;
+}
+
+void oracle_digest_keys(const uint64_t* keys, int64_t m, uint64_t* out) {
+  uint64_t s1 = 0, s2 = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    s1 += mix64(keys[i]);
+    s2 += mix64(keys[i] + DIGEST_K2);
+  }
+  out[0] = (uint64_t)m;
+  out[1] = s1;
+  out[2] = s2;
+}
+
+/* out[0] = |R|, out[1] = s1, out[2] = s2, out[3] = largest row. */
+int oracle_digest(const double* x, int64_t n, int d, int64_t ld, int k, double eps, int threads,
+                  uint64_t* out) {
+  grid_t g;
+  if (k < 1 || k > MAXK || build_grid(x, n, d, ld, k, eps, &g) != 0) return -1;
+  const double eps_sq = eps * eps;
+  int max_nb = 1;
+  for (int t = 0; t < k; ++t) max_nb *= 3;
+  uint64_t cnt = 0, s1 = 0, s2 = 0, mx = 0;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel reduction(+ : cnt, s1, s2) reduction(max : mx)
+#endif
+  {
+    int64_t* nb = (int64_t*)malloc(sizeof(int64_t) * max_nb);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t ci = 0; ci < g.n_cells; ++ci) {
+      const int nn = neighbours(&g, ci, nb);
+      for (int64_t qp = g.cstart[ci]; qp < g.cstart[ci + 1]; ++qp) {
+        const uint32_t q = g.order[qp];
+        const double* a = x + (int64_t)q * ld;
+        uint64_t row = 0;
+        for (int m = 0; m < nn; ++m)
+          for (int64_t cp = g.cstart[nb[m]]; cp < g.cstart[nb[m] + 1]; ++cp) {
+            const uint32_t c = g.order[cp];
+            if (direct_le_exit(a, x + (int64_t)c * ld, d, eps_sq)) {
+              const uint64_t key = ((uint64_t)q << 32) | c;
+              s1 += mix64(key);
+              s2 += mix64(key + DIGEST_K2);
+              ++row;
+            }
+          }
+        cnt += row;
+        if (row > mx) mx = row;
+      }
+    }
+    free(nb);
+  }
+  out[0] = cnt;
+  out[1] = s1;
+  out[2] = s2;
+  out[3] = mx;
+  free_grid(&g);
+  return 0;
+}

@@ -60,6 +60,7 @@ SIGNATURES = {
     "tj_cell_costs": (_i32, [_vp, _vp]),
     "tj_pair_sq_dists": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp]),
     "tj_write_pairs": (_i32, [ctypes.c_char_p, _vp, _i64, _vp, _vp, _i32]),
+    "tj_expand_pairs": (_i32, [_vp, _i64, _vp, _vp, _i32]),
     "tj_column_moments": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _vp]),
     "tj_permute_columns": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _i64, _vp]),
     "tj_brute_force": (_i32, [_vp, _vp, _i64, _i32, _i64, _f64, _vp, _vp, _vp, _vp]),
@@ -279,6 +280,23 @@ def write_pairs(path, offsets, neighbors, sq, threads: int | None = None) -> Non
                             nb.ctypes.data, sq.ctypes.data, int(th))
     if st != TJ_OK:
         _raise(st, lib.tj_last_error(None).decode())
+
+
+def expand_pairs(offsets, neighbors, threads: int | None = None):
+    """(m, 2) int64 (query id, neighbour id) rows of a host CSR (native, multi-threaded)."""
+    import numpy as np
+
+    lib = load_library()
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    m = int(off[-1])
+    nb = np.ascontiguousarray(neighbors[:m]).view(np.uint32) if m else np.zeros(1, np.uint32)
+    out = np.empty((m, 2), dtype=np.int64)
+    th = threads or min(32, os.cpu_count() or 1)
+    st = lib.tj_expand_pairs(off.ctypes.data, len(off) - 1, nb.ctypes.data, out.ctypes.data,
+                             int(th))
+    if st != TJ_OK:
+        _raise(st, lib.tj_last_error(None).decode())
+    return out
 
 
 def launch_count() -> int:

@@ -446,6 +446,15 @@ int tj_write_pairs(const char* path, const int64_t* offsets, int64_t n,
   });
 }
 
+int tj_expand_pairs(const int64_t* offsets, int64_t n, const uint32_t* neighbors, int64_t* out,
+                    int32_t threads) {
+  if (!offsets || n < 0 || !out) return TJ_EINVAL;
+  return guarded(nullptr, [&] {
+    if (offsets[n] > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
+    expand_pairs(offsets, n, neighbors, out, threads);
+  });
+}
+
 int tj_column_moments(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64_t ld,
                       double* mean, double* var, void* stream) {
   if (!ctx || !coords || !mean || !var) return TJ_EINVAL;

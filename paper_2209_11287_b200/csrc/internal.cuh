@@ -164,6 +164,8 @@ void launch_pair_sq_dists(const double* x, int64_t ld, int d, const int64_t* off
                           const uint32_t* nbr, int64_t m, double* out, cudaStream_t s);
 void write_pairs_file(const char* path, const int64_t* offsets, int64_t n, const uint32_t* nbr,
                       const double* sq, int threads);
+void expand_pairs(const int64_t* offsets, int64_t n, const uint32_t* nbr, int64_t* out,
+                  int threads);
 void column_moments(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld, double* h_mean,
                     double* h_var, cudaStream_t s);
 void permute_columns(const double* src, int64_t n, int d, int64_t ld, const int* h_perm,

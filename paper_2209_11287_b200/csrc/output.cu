@@ -52,6 +52,7 @@ void launch_pair_sq_dists(const double* x, int64_t ld, int d, const int64_t* off
 // printed like Python's f"{s:.17g}" (C's %.17g: the same correctly rounded
 // digits and exponent rule).  Pairs are formatted in blocks by a pool of host
 // threads and written in order.
+#include <algorithm>
 #include <cstdio>
 #include <thread>
 
@@ -96,6 +97,34 @@ void write_pairs_file(const char* path, const int64_t* offsets, int64_t n, const
       }
   }
   if (std::fclose(f) != 0) fail(TJ_EINVAL, std::string("error closing ") + path);
+}
+
+}  // namespace tj
+
+// ------------------------------------------------------------ (m, 2) pairs
+// JoinResult.pairs (join.py:80-91): the CSR expanded into (query id, neighbour
+// id) int64 rows.  Host threads take contiguous row ranges of ~equal pair count
+// and write (and first-touch) their own part of the output.
+namespace tj {
+
+void expand_pairs(const int64_t* offsets, int64_t n, const uint32_t* nbr, int64_t* out,
+                  int threads) {
+  const int64_t m = offsets[n];
+  const int T = int(std::max<int64_t>(1, std::min<int64_t>(threads, m / (int64_t(1) << 16) + 1)));
+  std::vector<int64_t> rstart(T + 1, n);
+  rstart[0] = 0;
+  for (int t = 1; t < T; ++t)  // first row whose pairs start at or after t*m/T
+    rstart[t] = std::lower_bound(offsets, offsets + n + 1, m / T * t) - offsets;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      for (int64_t r = std::min(rstart[t], n); r < std::min(rstart[t + 1], n); ++r)
+        for (int64_t e = offsets[r]; e < offsets[r + 1]; ++e) {
+          out[2 * e] = r;
+          out[2 * e + 1] = int64_t(nbr[e]);
+        }
+    });
+  for (auto& th : pool) th.join();
 }
 
 }  // namespace tj

@@ -89,41 +89,59 @@ class JoinStats:
         }
 
 
+class _PairsField:
+    """`JoinResult.pairs` as a dataclass field that is built on first read.
+
+    Assigned explicitly (the reference's constructor, join.py:80-91), it is a
+    plain value.  Left unset by the engine, the first read expands the CSR with
+    the native multi-threaded tj_expand_pairs and caches the array.
+    """
+
+    def __set_name__(self, owner, name):
+        self.slot = "_" + name
+
+    def __get__(self, obj, owner=None):
+        if obj is None:
+            return None  # the dataclass default
+        value = obj.__dict__.get(self.slot)
+        if value is None and obj.__dict__.get("offsets") is not None:
+            value = _native.expand_pairs(obj.offsets, obj.neighbors)
+            obj.__dict__[self.slot] = value
+        return value
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.slot] = None if value is None else np.asarray(value)
+
+
+@dataclass
 class JoinResult:
     """Pair set of the join: ordered (query id, neighbour id), self-pairs included.
 
-    The primary form is CSR: ``offsets`` (int64, n+1) and ``neighbors`` (int32,
-    ascending within each row), i.e. per-point neighbour lists.  ``pairs`` is the
-    reference's (m, 2) int64 array sorted by (query, neighbour) (join.py:80-91),
-    materialised on first access.
+    The reference's dataclass (join.py:80-91): ``pairs`` (m, 2) int64 sorted by
+    (query, neighbour), ``total_pairs``, ``selectivity`` = (|R| - n) / n,
+    ``stats``.  The engine fills the CSR form -- ``offsets`` (int64, n+1) and
+    ``neighbors`` (int32, ascending within each row), i.e. per-point neighbour
+    lists -- and ``pairs`` is expanded from it on first access.  A result built
+    from ``pairs`` alone (as reference callers do) derives the CSR on demand.
     """
 
-    __slots__ = ("offsets", "neighbors", "total_pairs", "selectivity", "stats", "_pairs")
+    pairs: np.ndarray = _PairsField()
+    total_pairs: int = 0
+    selectivity: float = 0.0
+    stats: JoinStats = field(default_factory=JoinStats)
+    offsets: np.ndarray | None = field(default=None, repr=False, compare=False)
+    neighbors: np.ndarray | None = field(default=None, repr=False, compare=False)
 
-    def __init__(self, offsets, neighbors, total_pairs, selectivity, stats):
-        self.offsets = offsets
-        self.neighbors = neighbors
-        self.total_pairs = int(total_pairs)
-        self.selectivity = float(selectivity)
-        self.stats = stats
-        self._pairs = None
-
-    @property
-    def pairs(self) -> np.ndarray:
-        if self._pairs is None:
-            n = len(self.offsets) - 1
-            counts = np.diff(self.offsets)
-            out = np.empty((self.total_pairs, 2), dtype=np.int64)
-            out[:, 0] = np.repeat(np.arange(n, dtype=np.int64), counts)
-            out[:, 1] = self.neighbors[: self.total_pairs]
-            self._pairs = out
-        return self._pairs
+    def __post_init__(self):
+        if self.offsets is None and self.__dict__.get("_pairs") is not None:
+            pr = self.__dict__["_pairs"]
+            n = int(pr[:, 0].max()) + 1 if len(pr) else 0
+            self.offsets = np.concatenate(
+                [[0], np.cumsum(np.bincount(pr[:, 0], minlength=n))]).astype(np.int64)
+            self.neighbors = pr[:, 1].astype(np.int32)
 
     def neighbors_of(self, i: int) -> np.ndarray:
-        return self.neighbors[self.offsets[i] : self.offsets[i + 1]]
-
-    def __repr__(self) -> str:
-        return f"JoinResult(total_pairs={self.total_pairs}, selectivity={self.selectivity:.4f})"
+        return self.neighbors[self.offsets[i]: self.offsets[i + 1]]
 
 
 @dataclass(frozen=True)
@@ -440,4 +458,5 @@ def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) 
     stats.index_seconds = t_indexed - t_start
     stats.refine_seconds = t_end - t_indexed
     stats.total_seconds = t_end - t_start
-    return JoinResult(offsets, neighbors, total, (total - dataset.n) / dataset.n, stats)
+    return JoinResult(total_pairs=total, selectivity=(total - dataset.n) / dataset.n, stats=stats,
+                      offsets=offsets, neighbors=neighbors)

@@ -1,9 +1,9 @@
 """GPU brute-force verification (the reference's oracle.brute_force_join, oracle.py:55-86).
 
 Every ordered pair is decided by the reference direct form on the GPU
-(tj_brute_force), independently of the grid index, so `verify` can check the
-indexed join far beyond the CPU oracle's 50,000-point guard
-(oracle.BRUTE_FORCE_GUARD, cli.py:165-171).
+(tj_brute_force), independently of the grid index.  The default guard is the
+reference's (oracle.BRUTE_FORCE_GUARD = 50,000, cli.py:165-171); with
+force=True the GPU checks inputs far beyond what the CPU oracle can.
 """
 
 from __future__ import annotations
@@ -15,8 +15,9 @@ from .datasets import as_dataset
 from .errors import ResourceError, ValidationError
 from .join import JoinResult, JoinStats
 
-# All-pairs work the GPU brute force takes without force=True (n^2 ordered pairs).
-GPU_BRUTE_FORCE_GUARD = 4_000_000
+# Largest n verified without force=True: the reference's guard (oracle.py:22), so
+# `verify` refuses the same inputs; with force=True the GPU takes any n.
+BRUTE_FORCE_GUARD = 50_000
 
 
 def brute_force_join(dataset, epsilon: float, force: bool = False,
@@ -27,9 +28,9 @@ def brute_force_join(dataset, epsilon: float, force: bool = False,
     ds = as_dataset(dataset)
     if not np.isfinite(epsilon) or epsilon <= 0:
         raise ValidationError(f"epsilon must be positive and finite, got {epsilon}")
-    if ds.n > GPU_BRUTE_FORCE_GUARD and not force:
+    if ds.n > BRUTE_FORCE_GUARD and not force:
         raise ResourceError(
-            f"n={ds.n} exceeds the GPU verification guard of {GPU_BRUTE_FORCE_GUARD}; "
+            f"n={ds.n} exceeds the verification guard of {BRUTE_FORCE_GUARD}; "
             "pass force=True to run anyway")
     ctx = _native.context(device)
     dev = f"cuda:{ctx.device}"
@@ -41,7 +42,8 @@ def brute_force_join(dataset, epsilon: float, force: bool = False,
     off = offsets.cpu().numpy()
     nb = nbr[:total].cpu().numpy()
     stats = JoinStats(candidates_refined=ds.n * ds.n, pairs_emitted=total)
-    return JoinResult(off, nb, total, (total - ds.n) / ds.n, stats)
+    return JoinResult(total_pairs=total, selectivity=(total - ds.n) / ds.n, stats=stats,
+                      offsets=off, neighbors=nb)
 
 
 def pair_set_diff(reference: JoinResult, engine: JoinResult):

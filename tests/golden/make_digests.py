@@ -1,0 +1,58 @@
+"""Full-set pair digests of the BASELINE configs from the golden-pinned C oracle.
+
+    python tests/golden/make_digests.py [config ...]   ->  tests/golden/full_digests.json
+
+The oracle (oracle/direct_join.c, the reference grid + direct form restated in C
+with -ffp-contract=off) is pinned against the reference itself by the other
+fixtures here (sweep.json, config1.json, sampled.*).  This script runs it over
+the FULL inputs of configs 1, 2, 3, 4 (d = 2, 4, 8) and 5 and records the
+order-independent digest of each pair set (count, two 64-bit sums of
+splitmix64(q << 32 | c); tests/digest.py), so the GPU suite can check the whole
+pair set at full size without a multi-GB fixture.  Configs 4 d >= 16 are
+brute force over 4e12 candidate pairs -- beyond this container's 8 cores; their
+full-size check is the GPU's exact direct-form brute force (tj_brute_force),
+itself pinned to the oracle at small n, plus the reference's sampled rows.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+
+import oracle  # noqa: E402
+from paper_2209_11287_b200.datasets import GenSpec, generate  # noqa: E402
+
+CONFIGS = {
+    "c1": ("uniform", 100_000, 2, 0.0143667),
+    "c2": ("uniform", 2_000_000, 4, 0.051306),
+    "c4d2": ("uniform", 2_000_000, 2, 0.00320714),
+    "c5": ("uniform", 50_000_000, 4, 0.0232204),
+    "c4d8": ("uniform", 2_000_000, 8, 0.244686),
+    "c3": ("exponential", 5_000_000, 8, 0.0118508),
+}
+
+
+def main(names):
+    path = HERE / "full_digests.json"
+    out = json.loads(path.read_text()) if path.exists() else {}
+    for name in names or list(CONFIGS):
+        dist, n, d, eps = CONFIGS[name]
+        ds = generate(GenSpec(dist, n, d, seed=0))
+        t = time.perf_counter()
+        dg = oracle.digest(ds, eps)
+        dg.update({"dist": dist, "n": n, "d": d, "eps": eps, "checksum": ds.checksum(),
+                   "oracle_seconds": round(time.perf_counter() - t, 1),
+                   "oracle_threads": oracle.num_threads()})
+        out[name] = dg
+        print(name, dg, flush=True)
+        path.write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

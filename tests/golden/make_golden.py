@@ -120,7 +120,7 @@ def sampled(name, n_random=10, q_per_cell=12, seed=0):
     big = np.argsort(-sizes, kind="stable")[: 50]
     cand_big = np.array([len(candidates_for_cell(idx, idx.ordered_cells[i])) for i in big])
     costliest = big[np.argsort(-(sizes[big] * cand_big), kind="stable")[:10]]
-    randoms = rng.choice(len(sizes), size=n_random, replace=False)
+    randoms = rng.choice(len(sizes), size=min(n_random, len(sizes)), replace=False)
     cells = list(dict.fromkeys([int(c) for c in costliest] + [int(c) for c in randoms]))
     refiner = _ScalarRefiner(ds, eps * eps, short_circuit=True)
     qids_all, counts, nbrs = [], [], []
@@ -147,8 +147,15 @@ def sampled(name, n_random=10, q_per_cell=12, seed=0):
         np.concatenate(nbrs).astype(np.int64) if nbrs else np.zeros(0, np.int64))
 
 
+SAMPLED = ("c2", "c3", "c4d2", "c4d8", "c4d16", "c4d32", "c4d64", "c5")
+
+
 def main(argv):
     which = set(argv[1:]) or {"generator", "sweep", "config1", "sampled"}
+    # "sampled:c4d2,c4d32" regenerates only those configs' rows, keeping the rest
+    only = [w.split(":", 1)[1].split(",") for w in which if w.startswith("sampled:")]
+    if only:
+        which.add("sampled")
     if "generator" in which:
         gen = {}
         for name, (dist, n, d, eps) in CONFIGS.items():
@@ -165,12 +172,19 @@ def main(argv):
     if "config1" in which:
         (HERE / "config1.json").write_text(json.dumps(config1(), indent=1))
     if "sampled" in which:
-        metas, arrays = [], {}
-        for name in ("c2", "c3", "c4d8", "c4d16", "c5"):
-            meta, q, c, nb = sampled(name)
-            metas.append(meta)
+        names = [n for grp in only for n in grp] if only else list(SAMPLED)
+        metas, arrays = {}, {}
+        if only and (HERE / "sampled.json").exists():
+            metas = {m["config"]: m for m in json.loads((HERE / "sampled.json").read_text())}
+            arrays = dict(np.load(HERE / "sampled.npz"))
+        for name in names:
+            # d >= 32 is one brute-force cell: the reference refiner takes ~1-3 s per query
+            q_per_cell = 12 if CONFIGS[name][2] < 32 else 24
+            meta, q, c, nb = sampled(name, q_per_cell=q_per_cell)
+            metas[name] = meta
             arrays[f"{name}_qids"], arrays[f"{name}_counts"], arrays[f"{name}_nbrs"] = q, c, nb
-        (HERE / "sampled.json").write_text(json.dumps(metas, indent=1))
+        order = [n for n in SAMPLED if n in metas]
+        (HERE / "sampled.json").write_text(json.dumps([metas[n] for n in order], indent=1))
         np.savez_compressed(HERE / "sampled.npz", **arrays)
 
 

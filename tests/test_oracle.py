@@ -107,3 +107,40 @@ def test_oracle_known_answers():
     assert oracle.csr_to_pairs(off, nb).tolist() == [[0, 0]]
     # kernels.py known answers: 3-4-5
     assert oracle.sqdist(Dataset([[0.0, 0.0], [3.0, 4.0]]), 0, 1) == 25.0
+
+
+def test_digest_implementations_agree():
+    """oracle_digest (C, streaming), tests/digest.py numpy and torch: one digest."""
+    import torch
+
+    from digest import csr_digest_numpy, csr_digest_torch, keys_digest_torch
+
+    ds = generate(GenSpec("exponential", 3000, 3, seed=9))
+    off, nb = oracle.join_csr(ds, 0.04)
+    want = oracle.digest(ds, 0.04)
+    got_np = csr_digest_numpy(off, nb)
+    got_t = csr_digest_torch(torch.from_numpy(off), torch.from_numpy(nb.astype(np.int32)))
+    assert got_t.pop("ascending")
+    assert got_np == got_t == want
+    keys = (oracle.csr_to_pairs(off, nb)[:, 0].astype(np.uint64) << np.uint64(32)) | nb.astype(np.uint64)
+    kd = oracle.digest_keys(keys)
+    assert kd == {k: want[k] for k in ("pairs", "s1", "s2")}
+    assert keys_digest_torch(torch.from_numpy(keys.view(np.int64))) == kd
+
+
+def test_full_digest_fixture_pinned_to_reference_config1():
+    """full_digests.json's c1 entry is the digest of the reference's own config-1 pair set
+    (config1.json SHA-256 of the reference self_join pairs)."""
+    import json
+
+    from digest import csr_digest_numpy
+
+    full = json.loads((oracle.HERE.parent / "tests" / "golden" / "full_digests.json").read_text())
+    c1 = load_json("config1.json")
+    ds = generate(GenSpec("uniform", 100_000, 2, seed=0))
+    off, nb = oracle.join_csr(ds, c1["eps"])
+    assert sha_pairs(oracle.csr_to_pairs(off, nb)) == c1["scalar"]["sha_pairs"]
+    dg = csr_digest_numpy(off, nb)
+    for key in ("pairs", "s1", "s2", "max_row"):
+        assert dg[key] == full["c1"][key]
+    assert full["c2"]["pairs"] == 129_482_252 and full["c5"]["pairs"] == 3_524_665_904
