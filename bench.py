@@ -12,8 +12,10 @@ reference's JoinStats.candidates_refined) with inputs resident in HBM; the
 step time in seconds is `ms_per_step`/1000 ("self-join s").  `e2e` repeats
 the measurement through the public API `self_join(host Dataset, JoinConfig)`
 with H2D of the coordinates and D2H of the CSR pair set inside the timed
-region.  N>1 ranks (torchrun) broadcast the dataset over NCCL and split the
-cells by estimated cost; times are the max over ranks.
+region.  N>1 ranks (torchrun) default to config 5 strong-scaled: each rank
+holds a 1/N row slice, the step plans equal-cost bin ranges (NCCL all-reduces),
+all-gathers the coordinates, joins its bins' cells and all-reduces the per-id
+counts into the global offsets (distributed.py); times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -362,7 +364,6 @@ def run_ours(args, world, rank, local):
 
     from paper_2209_11287_b200 import _native
     from paper_2209_11287_b200.datasets import Dataset, GenSpec, generate
-    from paper_2209_11287_b200.distributed import balanced_cell_ranges, broadcast_dataset
     from paper_2209_11287_b200.join import DeviceJoin, JoinConfig, self_join
 
     dist_name, n, d, eps = CONFIGS[args.config]
@@ -373,28 +374,21 @@ def run_ours(args, world, rank, local):
         ds, n_own, (c_lo, c_hi) = weak_local_dataset(dist_name, n, d, eps, rank, world)
         n = ds.n
     else:
-        ds = generate(GenSpec(dist_name, n, d, seed=0)) if rank == 0 else None
+        ds = generate(GenSpec(dist_name, n, d, seed=0))
     cfg = JoinConfig(epsilon=eps, kernel=args.kernel, short_circuit=not args.no_short_circuit,
                      device=dev)
     # device-resident input on rank 0 (strong: other ranks receive it inside the
     # step) or on every rank (weak: its own slab + halo)
-    coords0 = torch.from_numpy(ds.coords).to(f"cuda:{dev}") if (rank == 0 or weak) else None
+    coords0 = torch.from_numpy(ds.coords).to(f"cuda:{dev}")
     weak_range = {}  # owned cell range of the (deterministic) local grid, found once
     dp = 4 * ((d + 3) // 4)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream(dev)
 
     def one_step(kernel_cfg, timings=None):
-        import torch.distributed as dist
-
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
-        if world > 1 and not weak:
-            coords = coords0 if rank == 0 else torch.empty((n, dp), dtype=torch.float64,
-                                                            device=f"cuda:{dev}")
-            dist.broadcast(coords, src=0)
-        else:
-            coords = coords0
+        coords = coords0  # N = 1, or weak: this rank's slab + halo, resident
         ev[1].record(stream)
         # non-root ranks hold only the shape on the host (np.empty touches no pages)
         work = ds if ds is not None else Dataset._wrap(np.empty((n, dp)), d)
@@ -410,9 +404,6 @@ def run_ours(args, world, rank, local):
                 weak_range["r"] = (cb, ce)
                 weak_range["C"] = int(job.ctx.cell_costs(info.n_cells)[cb:ce].sum())
             cell_range = weak_range["r"]
-        elif world > 1:
-            costs = job.ctx.cell_costs(info.n_cells)
-            cell_range = balanced_cell_ranges(costs, world)[rank]
         job.refine(cell_range=cell_range)
         refine_ms = job.ctx.last_refine_ms()
         ev[3].record(stream)
@@ -528,22 +519,6 @@ def run_ours(args, world, rank, local):
         e2e_val = 2.0 * d * C / e2e_s / 1e12
         h2d = int(sum_over_ranks(float(ds.coords.nbytes), world))
         d2h = int(sum_over_ranks(float(off_h.nbytes + nbr_h.nbytes), world))
-    else:
-        from paper_2209_11287_b200.distributed import shard_self_join
-
-        ts = []
-        for i in range(args.warmup + args.steps):
-            barrier(world)
-            t = time.perf_counter()
-            _, host_csr, _ = shard_self_join(ds, cfg)
-            el = max_over_ranks(time.perf_counter() - t, world)
-            if i >= args.warmup:
-                ts.append(el)
-        e2e_s = float(np.mean(ts))
-        e2e_val = 2.0 * d * C / e2e_s / 1e12
-        if host_csr is not None:
-            d2h = host_csr[0].nbytes + host_csr[1].nbytes
-
     if rank != 0:
         return
     cpu = None
@@ -588,13 +563,157 @@ def run_ours(args, world, rank, local):
                 "api": "self_join(host Dataset, JoinConfig) -> CSR in pinned host memory"
                        if world == 1 else
                        "per rank: DeviceJoin over its slab + halo (H2D, join of its cells, D2H "
-                       "of its rows); max over ranks" if weak else
-                       "distributed.shard_self_join (NCCL bcast, device-side CSR combine, one "
-                       "D2H on rank 0)"},
+                       "of its rows); max over ranks"},
         "gpu_launches": launches,
         "guard_rechecks": timings[0]["rechecks"],
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_strong(args, world, rank, local):
+    """N > 1, strong scaling (the default): ONE workload (config 5 unless --config)
+    split by estimated cost over the ranks with the strong layout of
+    distributed.py -- every step all-reduces the bin bounds/histogram, all-gathers
+    the coordinates (NCCL), selects each rank's bins + halo on the device, builds
+    the local grid, refines the owned cells, emits canonical rows and all-reduces
+    the per-id counts into the global CSR offsets.  Inputs at step start: each
+    rank's 1/N row slice resident on its device.  Times are CUDA events on each
+    rank, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_11287_b200 import _native
+    from paper_2209_11287_b200.datasets import GenSpec, generate
+    from paper_2209_11287_b200.distributed import (
+        SharedHostCSR,
+        assemble_host_csr,
+        row_slice,
+        strong_self_join,
+    )
+    from paper_2209_11287_b200.join import JoinConfig
+
+    dist_name, n, d, eps = CONFIGS[args.config]
+    dev = local
+    torch.cuda.set_device(dev)
+    ds = generate(GenSpec(dist_name, n, d, seed=0))  # each host process reads its slice from it
+    a, b = row_slice(n, rank, world)
+    host_rows = torch.from_numpy(ds.coords[a:b]).pin_memory()
+    rows = host_rows.to(f"cuda:{dev}")
+    cfg = JoinConfig(epsilon=eps, kernel=args.kernel, short_circuit=not args.no_short_circuit,
+                     device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream(dev)
+    phases = ("plan", "gather", "select", "index", "refine", "offsets")
+
+    def one_step(timings=None):
+        evs = {"start": torch.cuda.Event(enable_timing=True)}
+        evs["start"].record(stream)
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            evs[name] = e
+
+        shard = strong_self_join(rows, n, d, cfg, timer=mark)
+        torch.cuda.synchronize(dev)
+        if timings is not None:
+            st = shard.job.ctx.stats()
+            t, prev = {}, "start"
+            for ph in phases:
+                t[ph + "_ms"] = evs[prev].elapsed_time(evs[ph])
+                prev = ph
+            t["step_ms"] = evs["start"].elapsed_time(evs["offsets"])
+            t["refine_kernel_ms"] = shard.job.ctx.last_refine_ms() if shard.pairs else 0.0
+            t["rank_candidates"] = int(st.candidates_refined)
+            t["rank_pairs"] = shard.pairs
+            t["pairs"] = shard.total_pairs
+            t["n_local"] = shard.n_local
+            timings.append(t)
+        return shard
+
+    with ClockSampler(dev) as clk:
+        clk.wait_first()
+        t_w = time.monotonic()
+        for _ in range(max(args.warmup, 3)):
+            one_step()
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        launches0 = _native.launch_count()
+        timings = []
+        for _ in range(args.steps):
+            one_step(timings)
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        launches = _native.launch_count() - launches0
+        clk.window = (t_w, time.monotonic())
+        time.sleep(0.25)
+    mean = lambda k: float(np.mean([t[k] for t in timings]))
+    step_ms = max_over_ranks(mean("step_ms"), world)
+    phase_max = {ph: max_over_ranks(mean(ph + "_ms"), world) for ph in phases}
+    C = int(round(sum_over_ranks(float(timings[0]["rank_candidates"]), world)))
+    value = 2.0 * d * C / (step_ms * 1e-3) / 1e12
+    ref_ms = mean("refine_kernel_ms")
+    achieved = 2.0 * d * timings[0]["rank_candidates"] / max(ref_ms * 1e-3, 1e-12) / 1e12
+    peak_dmma, _ = _native.fp64_peak(1)
+    peak_dfma, _ = _native.fp64_peak(0)
+    peak = max(peak_dmma, peak_dfma)
+
+    # e2e: each rank uploads its row slice (pinned), runs the step, and writes its
+    # rows into the shared page-locked host CSR; root also copies the offsets
+    total = timings[0]["pairs"]
+    shared = SharedHostCSR(total)
+    ts = []
+    for i in range(args.warmup + args.steps):
+        barrier(world)
+        t = time.perf_counter()
+        r_dev = host_rows.to(f"cuda:{dev}", non_blocking=True)
+        shard = strong_self_join(r_dev, n, d, cfg)
+        csr = assemble_host_csr(shard, shared)
+        el = max_over_ranks(time.perf_counter() - t, world)
+        if i >= args.warmup:
+            ts.append(el)
+    shared.close()
+    e2e_s = float(np.mean(ts))
+    nbytes_h2d = int(sum_over_ranks(float(host_rows.numel() * 8), world))
+    if rank != 0:
+        return
+    assert csr is not None and int(csr[0][-1]) == total
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "self_join_s": step_ms / 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)",
+        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps,
+                   "kernel": args.kernel, "short_circuit": cfg.short_circuit,
+                   "candidate_pairs": C, "result_pairs": total,
+                   "l2": "256 MiB write between steps",
+                   "parallelism": f"strong: one workload, {world} ranks own equal-cost "
+                                  "contiguous (x0, x1) bin ranges; NCCL all-reduce of bounds, "
+                                  "histogram and per-id counts + all-gather of the coordinates "
+                                  "inside the step"},
+        "phases_ms_max_over_ranks": phase_max,
+        "rank0": {"n_local": timings[0]["n_local"], "pairs": timings[0]["rank_pairs"],
+                  "refine_kernel_ms": ref_ms},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": refine_kernel_name(args.kernel, d) + " (rank 0)",
+                     "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, "
+                                    f"DFMA {peak_dfma:.2f}) TFLOP/s",
+                     "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))"},
+        "e2e": {"value": 2.0 * d * C / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
+                "h2d_bytes_per_step": nbytes_h2d,
+                "d2h_bytes_per_step": 8 * (n + 1) + 4 * total,
+                "api": "distributed.strong_self_join + assemble_host_csr (each rank uploads its "
+                       "row slice and writes its rows into one shared mapped host CSR)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": None,
         "host": host_info(),
     }
     print(json.dumps(line), flush=True)
@@ -606,19 +725,24 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
+                    help="workload (default: c2 on one GPU, c5 strong-scaled over N > 1)")
     ap.add_argument("--kernel", choices=("tile", "scalar"), default="tile")
     ap.add_argument("--no-short-circuit", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
-                    help="N > 1: weak = each rank owns one workload-sized slab (default, the "
-                         "path shards with no collective); strong = one workload split by cost")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="strong",
+                    help="N > 1: strong = one workload (default c5) split by estimated cost "
+                         "(the default); weak = each rank owns one workload-sized slab")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of host-core reference work per run (sampled cells)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
+    if args.config is None:
+        args.config = "c5" if world > 1 and args.scaling == "strong" else "c2"
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif world > 1 and args.scaling == "strong":
+        run_strong(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
     if world > 1:

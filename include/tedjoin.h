@@ -178,6 +178,58 @@ int tj_brute_force(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int6
                    double eps, int64_t* offsets, uint32_t* neighbors, int64_t* total,
                    void* stream);
 
+/* ---- page-locked host memory ---------------------------------------------------- */
+/* Page-lock a host range (cudaHostRegister, portable; mapped != 0 also maps it
+ * into the device address space and returns the device alias in *device_ptr,
+ * which may be NULL).  A range that is already page-locked is accepted as is;
+ * failures never leave a stale CUDA error behind.  Synchronous. */
+int tj_host_register(void* ptr, int64_t bytes, int32_t mapped, void** device_ptr);
+int tj_host_unregister(void* ptr);
+
+/* ---- multi-GPU strong layout: cell-partitioned shards of one join ----------------
+ * Replaces the reference's data-parallel executor (join.py:184-197, a thread pool
+ * over a batch's cells) with one process per GPU owning a contiguous, cost-balanced
+ * range of the lexicographic cell order.  Bins are the first
+ * `pdims` (1 or 2) indexed dims of a point's cell, b_j = floor(x_j/eps) - origin[j]
+ * (grid.py:81), numbered L = b_0*span[1] + b_1; a rank owns bins [own_lo, own_hi]
+ * (inclusive).  origin/span are host arrays of pdims entries. */
+/* floor(x_j/eps) bounds of coords (device rows, stride ld) -> host lo[pdims],
+ * hi[pdims].  Synchronous. */
+int tj_shard_bounds(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t pdims,
+                    double eps, int64_t* lo, int64_t* hi, void* stream);
+/* Points per bin -> device int64 hist[span0*span1] (zeroed first): the estimator's
+ * input (join.py:122-124) at bin granularity.  Asynchronous. */
+int tj_shard_histogram(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t pdims,
+                       double eps, const int64_t* origin, const int64_t* span, int64_t* hist,
+                       void* stream);
+/* Stable compaction of the points a rank needs: those whose bin is within
+ * Chebyshev distance 1 of an owned bin (its cells' candidates, grid.py:104-133).
+ * out: device (capacity, ld_out) f64, columns >= d zeroed; gid: device uint32
+ * (gid_base + row index of each kept point).  out == NULL only counts.
+ * *selected = kept points.  Synchronous. */
+int tj_shard_select(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t d,
+                    int32_t pdims, double eps, const int64_t* origin, const int64_t* span,
+                    int64_t own_lo, int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid,
+                    int64_t gid_base, int64_t capacity, int64_t* selected, void* stream);
+/* The owned cells [*cell_begin, *cell_end) of the grid built on ctx (lexicographic
+ * cell order, so contiguous).  Synchronous. */
+int tj_shard_cell_range(tj_ctx* ctx, int32_t pdims, const int64_t* origin, const int64_t* span,
+                        int64_t own_lo, int64_t own_hi, int64_t* cell_begin, int64_t* cell_end);
+/* ids[e] = gid[ids[e]] (device arrays): local neighbour ids -> global ids.  Async. */
+int tj_remap_ids(tj_ctx* ctx, uint32_t* ids, int64_t m, const uint32_t* gid, void* stream);
+/* counts[gid[l]] = offsets[l+1] - offsets[l] for the non-empty local rows (device).
+ * Summing the ranks' count arrays gives the global per-id counts.  Async. */
+int tj_scatter_counts(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const uint32_t* gid,
+                      int32_t* counts, void* stream);
+/* offsets[0..n] = exclusive prefix sum of counts[0..n-1] (device).  Async. */
+int tj_counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
+                         void* stream);
+/* Copy every non-empty local row l (neighbors already global ids) to
+ * dst[global_offsets[gid[l]] ...]; dst may be device memory or mapped pinned
+ * host memory (cudaHostRegisterMapped), so ranks write one shared host CSR.  Async. */
+int tj_place_rows(tj_ctx* ctx, const int64_t* offsets, const uint32_t* neighbors, int64_t n_rows,
+                  const uint32_t* gid, const int64_t* global_offsets, uint32_t* dst, void* stream);
+
 /* ---- measurement helpers ------------------------------------------------ */
 /* FP64 throughput microbenchmark on the current device: kind 0 = DFMA,
  * 1 = DMMA m8n8k4, 2 = both interleaved.  Reports FLOP/s counting 2 per FMA. */

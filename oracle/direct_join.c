@@ -76,9 +76,58 @@ static int build_grid(const double* x, int64_t n, int d, int64_t ld, int k, doub
     for (int t = 0; t < k; ++t) cc[i * k + t] = (int64_t)floor(x[i * ld + t] / eps);
     g->order[i] = (uint32_t)i;
   }
-  g_sort.cc = cc;
-  g_sort.k = k;
-  qsort(g->order, (size_t)n, sizeof(uint32_t), cmp_point);
+  /* stable lexicographic order (grid.py:83): when the k coordinate spans pack
+   * into 64 bits, an LSD radix sort of (packed key, id) -- ids ascending inside
+   * a cell because LSD passes are stable; otherwise qsort with the id tie-break. */
+  int64_t lo[MAXK], hi[MAXK];
+  int bits[MAXK], total_bits = 0;
+  for (int t = 0; t < k; ++t) {
+    lo[t] = INT64_MAX;
+    hi[t] = INT64_MIN;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int t = 0; t < k; ++t) {
+      const int64_t c = cc[i * k + t];
+      if (c < lo[t]) lo[t] = c;
+      if (c > hi[t]) hi[t] = c;
+    }
+  for (int t = 0; t < k; ++t) {
+    const uint64_t span = (uint64_t)(hi[t] - lo[t]);
+    bits[t] = 0;
+    while (bits[t] < 64 && (span >> bits[t]) != 0) ++bits[t];
+    total_bits += bits[t];
+  }
+  if (n > 1 && total_bits <= 64 && hi[0] - lo[0] >= 0) {
+    uint64_t* key = (uint64_t*)malloc(sizeof(uint64_t) * n);
+    uint64_t* key2 = (uint64_t*)malloc(sizeof(uint64_t) * n);
+    uint32_t* ord2 = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    for (int64_t i = 0; i < n; ++i) {
+      uint64_t kk = 0;
+      for (int t = 0; t < k; ++t)
+        kk = (bits[t] ? (kk << bits[t]) : kk) | (uint64_t)(cc[i * k + t] - lo[t]);
+      key[i] = kk;
+    }
+    for (int shift = 0; shift < total_bits; shift += 11) {
+      int64_t cnt[2049];
+      memset(cnt, 0, sizeof(cnt));
+      for (int64_t i = 0; i < n; ++i) ++cnt[((key[i] >> shift) & 2047) + 1];
+      for (int b = 0; b < 2048; ++b) cnt[b + 1] += cnt[b];
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t at = cnt[(key[i] >> shift) & 2047]++;
+        key2[at] = key[i];
+        ord2[at] = g->order[i];
+      }
+      uint64_t* tk = key; key = key2; key2 = tk;
+      uint32_t* to = g->order; g->order = ord2; ord2 = to;
+    }
+    free(key);
+    free(key2);
+    free(ord2);
+  } else {
+    g_sort.cc = cc;
+    g_sort.k = k;
+    qsort(g->order, (size_t)n, sizeof(uint32_t), cmp_point);
+  }
   g->cstart = (int64_t*)malloc(sizeof(int64_t) * (n + 1));
   g->ccoord = (int64_t*)malloc(sizeof(int64_t) * n * k);
   int64_t nc = 0;

@@ -64,6 +64,18 @@ SIGNATURES = {
     "tj_column_moments": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _vp]),
     "tj_permute_columns": (_i32, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _i64, _vp]),
     "tj_brute_force": (_i32, [_vp, _vp, _i64, _i32, _i64, _f64, _vp, _vp, _vp, _vp]),
+    "tj_host_register": (_i32, [_vp, _i64, _i32, ctypes.POINTER(_vp)]),
+    "tj_host_unregister": (_i32, [_vp]),
+    "tj_shard_bounds": (_i32, [_vp, _vp, _i64, _i64, _i32, _f64, _vp, _vp, _vp]),
+    "tj_shard_histogram": (_i32, [_vp, _vp, _i64, _i64, _i32, _f64, _vp, _vp, _vp, _vp]),
+    "tj_shard_select": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _f64, _vp, _vp, _i64, _i64,
+                               _vp, _i64, _vp, _i64, _i64, ctypes.POINTER(_i64), _vp]),
+    "tj_shard_cell_range": (_i32, [_vp, _i32, _vp, _vp, _i64, _i64, ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_i64)]),
+    "tj_remap_ids": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "tj_scatter_counts": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "tj_counts_to_offsets": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "tj_place_rows": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
     "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_last_refine_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
@@ -244,6 +256,73 @@ class Context:
             ctypes.byref(total) if neighbors is None else None, self.stream().cuda_stream))
         return int(total.value)
 
+    # ---- multi-GPU strong layout (shard.cu) ----
+    @staticmethod
+    def _bins(pdims, origin, span):
+        import numpy as np
+
+        o = np.ascontiguousarray(origin, dtype=np.int64)[:pdims]
+        sp = np.ascontiguousarray(span, dtype=np.int64)[:pdims]
+        return o, sp
+
+    def shard_bounds(self, coords, n: int, pdims: int, eps: float):
+        """(lo, hi) numpy int64[pdims]: floor(x_j / eps) bounds of the rows."""
+        import numpy as np
+
+        lo, hi = np.zeros(2, np.int64), np.zeros(2, np.int64)
+        self._check(self.lib.tj_shard_bounds(
+            self.handle, coords.data_ptr() if n else None, int(n), int(coords.stride(0)),
+            int(pdims), float(eps), lo.ctypes.data, hi.ctypes.data, self.stream().cuda_stream))
+        return lo[:pdims], hi[:pdims]
+
+    def shard_histogram(self, coords, n: int, pdims: int, eps: float, origin, span, hist):
+        o, sp = self._bins(pdims, origin, span)
+        self._check(self.lib.tj_shard_histogram(
+            self.handle, coords.data_ptr() if n else None, int(n), int(coords.stride(0)),
+            int(pdims), float(eps), o.ctypes.data, sp.ctypes.data, hist.data_ptr(),
+            self.stream().cuda_stream))
+
+    def shard_select(self, coords, n: int, d: int, pdims: int, eps: float, origin, span,
+                     own_lo: int, own_hi: int, out=None, gid=None, gid_base: int = 0) -> int:
+        o, sp = self._bins(pdims, origin, span)
+        sel = _i64()
+        self._check(self.lib.tj_shard_select(
+            self.handle, coords.data_ptr() if n else None, int(n), int(coords.stride(0)), int(d),
+            int(pdims), float(eps), o.ctypes.data, sp.ctypes.data, int(own_lo), int(own_hi),
+            out.data_ptr() if out is not None else None,
+            int(out.stride(0)) if out is not None else 0,
+            gid.data_ptr() if gid is not None else None, int(gid_base),
+            int(out.shape[0]) if out is not None else 0, ctypes.byref(sel),
+            self.stream().cuda_stream))
+        return int(sel.value)
+
+    def shard_cell_range(self, pdims: int, origin, span, own_lo: int, own_hi: int):
+        o, sp = self._bins(pdims, origin, span)
+        b, e = _i64(), _i64()
+        self._check(self.lib.tj_shard_cell_range(self.handle, int(pdims), o.ctypes.data,
+                                                 sp.ctypes.data, int(own_lo), int(own_hi),
+                                                 ctypes.byref(b), ctypes.byref(e)))
+        return int(b.value), int(e.value)
+
+    def remap_ids(self, ids, m: int, gid):
+        self._check(self.lib.tj_remap_ids(self.handle, ids.data_ptr() if m else None, int(m),
+                                          gid.data_ptr(), self.stream().cuda_stream))
+
+    def scatter_counts(self, offsets, n_rows: int, gid, counts):
+        self._check(self.lib.tj_scatter_counts(self.handle, offsets.data_ptr(), int(n_rows),
+                                               gid.data_ptr(), counts.data_ptr(),
+                                               self.stream().cuda_stream))
+
+    def counts_to_offsets(self, counts, n: int, offsets):
+        self._check(self.lib.tj_counts_to_offsets(self.handle, counts.data_ptr(), int(n),
+                                                  offsets.data_ptr(), self.stream().cuda_stream))
+
+    def place_rows(self, offsets, neighbors, n_rows: int, gid, global_offsets, dst_ptr: int):
+        self._check(self.lib.tj_place_rows(self.handle, offsets.data_ptr(), neighbors.data_ptr(),
+                                           int(n_rows), gid.data_ptr(),
+                                           global_offsets.data_ptr(), int(dst_ptr),
+                                           self.stream().cuda_stream))
+
     def last_refine_ms(self) -> float:
         ms = _f64()
         self._check(self.lib.tj_last_refine_ms(self.handle, ctypes.byref(ms)))
@@ -297,6 +376,24 @@ def expand_pairs(offsets, neighbors, threads: int | None = None):
     if st != TJ_OK:
         _raise(st, lib.tj_last_error(None).decode())
     return out
+
+
+def host_register(ptr: int, nbytes: int, mapped: bool = False) -> int | None:
+    """Page-lock host memory; returns the device alias when mapped (else None)."""
+    lib = load_library()
+    dptr = _vp()
+    st = lib.tj_host_register(ctypes.c_void_p(ptr), int(nbytes), int(bool(mapped)),
+                              ctypes.byref(dptr) if mapped else None)
+    if st != TJ_OK:
+        _raise(st, lib.tj_last_error(None).decode())
+    return int(dptr.value) if mapped else None
+
+
+def host_unregister(ptr: int) -> None:
+    lib = load_library()
+    st = lib.tj_host_unregister(ctypes.c_void_p(ptr))
+    if st != TJ_OK:
+        _raise(st, lib.tj_last_error(None).decode())
 
 
 def launch_count() -> int:

@@ -488,4 +488,125 @@ int tj_brute_force(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int6
   });
 }
 
+// ---- page-locked host memory -------------------------------------------------------
+int tj_host_register(void* ptr, int64_t bytes, int32_t mapped, void** device_ptr) {
+  if (!ptr || bytes <= 0) return TJ_EINVAL;
+  return guarded(nullptr, [&] {
+    unsigned flags = cudaHostRegisterPortable | (mapped ? cudaHostRegisterMapped : 0u);
+    cudaError_t e = cudaHostRegister(ptr, size_t(bytes), flags);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      (void)cudaGetLastError();  // already page-locked: usable as is, no stale error left behind
+    } else if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      fail(TJ_ECUDA, std::string("cudaHostRegister failed: ") + cudaGetErrorString(e));
+    }
+    if (device_ptr) {
+      *device_ptr = nullptr;
+      e = cudaHostGetDevicePointer(device_ptr, ptr, 0);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(TJ_ECUDA, std::string("cudaHostGetDevicePointer failed: ") + cudaGetErrorString(e));
+      }
+    }
+  });
+}
+
+int tj_host_unregister(void* ptr) {
+  if (!ptr) return TJ_EINVAL;
+  return guarded(nullptr, [&] {
+    cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      fail(TJ_ECUDA, std::string("cudaHostUnregister failed: ") + cudaGetErrorString(e));
+    }
+  });
+}
+
+// ---- multi-GPU strong layout (shard.cu) ----------------------------------------
+static void check_bins(int32_t pdims, const int64_t* origin, const int64_t* span) {
+  if (pdims < 1 || pdims > 2) fail(TJ_EINVAL, "pdims must be 1 or 2");
+  if (!origin || !span) fail(TJ_EINVAL, "origin / span is null");
+  for (int j = 0; j < pdims; ++j)
+    if (span[j] < 1) fail(TJ_EINVAL, "span entries must be >= 1");
+}
+
+int tj_shard_bounds(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t pdims,
+                    double eps, int64_t* lo, int64_t* hi, void* stream) {
+  if (!ctx || !lo || !hi) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (pdims < 1 || pdims > 2) fail(TJ_EINVAL, "pdims must be 1 or 2");
+    if (n > 0 && (!coords || ld < pdims)) fail(TJ_EINVAL, "need coords and ld >= pdims");
+    if (!(std::isfinite(eps) && eps > 0)) fail(TJ_EINVAL, "epsilon must be positive and finite");
+    shard_bounds(ctx, coords, n, ld, pdims, eps, lo, hi, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_shard_histogram(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t pdims,
+                       double eps, const int64_t* origin, const int64_t* span, int64_t* hist,
+                       void* stream) {
+  if (!ctx || !hist) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    check_bins(pdims, origin, span);
+    if (n > 0 && (!coords || ld < pdims)) fail(TJ_EINVAL, "need coords and ld >= pdims");
+    shard_histogram(coords, n, ld, pdims, eps, origin, span, hist,
+                    static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_shard_select(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t d,
+                    int32_t pdims, double eps, const int64_t* origin, const int64_t* span,
+                    int64_t own_lo, int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid,
+                    int64_t gid_base, int64_t capacity, int64_t* selected, void* stream) {
+  if (!ctx || !selected) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    check_bins(pdims, origin, span);
+    if (n > 0 && (!coords || ld < d || d < pdims)) fail(TJ_EINVAL, "need coords, ld >= d >= pdims");
+    if (out && (!gid || ld_out < d)) fail(TJ_EINVAL, "need gid and ld_out >= d with out");
+    *selected = shard_select(ctx, coords, n, ld, d, pdims, eps, origin, span, own_lo, own_hi, out,
+                             ld_out, gid, gid_base, capacity, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_shard_cell_range(tj_ctx* ctx, int32_t pdims, const int64_t* origin, const int64_t* span,
+                        int64_t own_lo, int64_t own_hi, int64_t* cell_begin, int64_t* cell_end) {
+  if (!ctx || !cell_begin || !cell_end) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    check_bins(pdims, origin, span);
+    if (pdims > ctx->g.k) fail(TJ_EINVAL, "pdims exceeds the grid's k_idx");
+    shard_cell_range(ctx, pdims, origin, span, own_lo, own_hi, cell_begin, cell_end,
+                     ctx->last_stream);
+  });
+}
+
+int tj_remap_ids(tj_ctx* ctx, uint32_t* ids, int64_t m, const uint32_t* gid, void* stream) {
+  if (!ctx || (m > 0 && (!ids || !gid))) return TJ_EINVAL;
+  return guarded(ctx, [&] { shard_remap_ids(ids, m, gid, static_cast<cudaStream_t>(stream)); });
+}
+
+int tj_scatter_counts(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const uint32_t* gid,
+                      int32_t* counts, void* stream) {
+  if (!ctx || (n_rows > 0 && (!offsets || !gid || !counts))) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    shard_scatter_counts(offsets, n_rows, gid, counts, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
+                         void* stream) {
+  if (!ctx || !offsets || (n > 0 && !counts) || n < 0) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    counts_to_offsets(ctx, counts, n, offsets, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_place_rows(tj_ctx* ctx, const int64_t* offsets, const uint32_t* neighbors, int64_t n_rows,
+                  const uint32_t* gid, const int64_t* global_offsets, uint32_t* dst, void* stream) {
+  if (!ctx || (n_rows > 0 && (!offsets || !gid || !global_offsets || !dst))) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    shard_place_rows(offsets, neighbors, n_rows, gid, global_offsets, dst,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
 }  // extern "C"

@@ -173,6 +173,24 @@ void permute_columns(const double* src, int64_t n, int d, int64_t ld, const int*
 void brute_force_join(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld, double eps,
                       int64_t* offsets, uint32_t* nbr, int64_t* total, cudaStream_t s);
 void build_window_cells(tj_ctx* ctx, cudaStream_t s);
+// shard.cu (multi-GPU strong layout)
+void shard_bounds(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int pdims, double eps,
+                  int64_t* lo, int64_t* hi, cudaStream_t s);
+void shard_histogram(const double* x, int64_t n, int64_t ld, int pdims, double eps,
+                     const int64_t* origin, const int64_t* span, int64_t* hist, cudaStream_t s);
+int64_t shard_select(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int pdims,
+                     double eps, const int64_t* origin, const int64_t* span, int64_t own_lo,
+                     int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid, int64_t gid_base,
+                     int64_t capacity, cudaStream_t s);
+void shard_cell_range(tj_ctx* ctx, int pdims, const int64_t* origin, const int64_t* span,
+                      int64_t own_lo, int64_t own_hi, int64_t* begin, int64_t* end, cudaStream_t s);
+void shard_remap_ids(uint32_t* ids, int64_t m, const uint32_t* gid, cudaStream_t s);
+void shard_scatter_counts(const int64_t* loff, int64_t n_rows, const uint32_t* gid, int32_t* counts,
+                          cudaStream_t s);
+void shard_place_rows(const int64_t* loff, const uint32_t* nbr, int64_t n_rows, const uint32_t* gid,
+                      const int64_t* goff, uint32_t* dst, cudaStream_t s);
+void counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
+                       cudaStream_t s);
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
                        unsigned long long* max_row, cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,

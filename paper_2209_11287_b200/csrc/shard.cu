@@ -1,0 +1,319 @@
+// Multi-GPU strong layout: cell-partitioned shards of one join.
+//
+// Replaces the reference's only data-parallel executor, a thread pool over a
+// batch's cells (join.py:184-197), with one process per GPU owning a
+// contiguous, cost-balanced range of the lexicographic cell order:
+//  * bins: the first `pdims` (<= 2) indexed dims of a point's cell,
+//    b_j = floor(x_j / eps) - origin_j (the grid's own IEEE division + floor,
+//    grid.py:81), numbered lexicographically L = b_0 * span_1 + b_1 -- the
+//    prefix of the reference's lexicographic cell order (grid.py:83);
+//  * a rank owns the bins [own_lo, own_hi] (inclusive, lexicographic), hence
+//    every grid cell whose prefix falls there -- one contiguous cell range;
+//  * it needs the points of its own bins plus the one-cell halo: a point is
+//    kept when some bin within Chebyshev distance 1 of its own is owned.  For
+//    a neighbour row q0 in {b0-1, b0, b0+1} the candidate bins are the
+//    lexicographic interval q0*span1 + [b1-1, b1+1] (clipped), so the test is
+//    three interval intersections;
+//  * the kept points are compacted stably, so local ids are monotone in global
+//    ids: cells, candidate lists and sorted rows of the local grid are exactly
+//    the global grid's for the owned cells (ids mapped through `gid`).
+// Kernels here: prefix bounds, prefix histogram (the estimator's input), the
+// halo select, the owned cell range of a local grid, id remapping, per-row
+// counts scattered to global ids, and row placement at global CSR offsets
+// (device memory or mapped pinned host memory).
+#include <climits>
+
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace tj {
+
+struct Bins {
+  int pdims;
+  long long origin0, origin1;
+  long long span0, span1;
+  double eps;
+};
+
+__device__ __forceinline__ long long bin_coord(double x, double eps) {
+  return __double2ll_rd(__ddiv_rn(x, eps));  // floor(x / eps), as grid.cu cell_coord
+}
+
+__device__ __forceinline__ void point_bins(const double* row, const Bins& b, long long& b0,
+                                           long long& b1) {
+  b0 = bin_coord(row[0], b.eps) - b.origin0;
+  b1 = b.pdims > 1 ? bin_coord(row[1], b.eps) - b.origin1 : 0;
+}
+
+// Does the Chebyshev-1 neighbourhood of bin (b0, b1) meet the owned interval?
+__device__ __forceinline__ bool bin_needed(long long b0, long long b1, const Bins& b,
+                                           long long lo, long long hi) {
+  bool need = false;
+#pragma unroll
+  for (int dq = -1; dq <= 1; ++dq) {
+    const long long q0 = b0 + dq;
+    if (q0 < 0 || q0 >= b.span0) continue;
+    const long long l = q0 * b.span1 + max(b1 - (b.pdims > 1 ? 1 : 0), 0ll);
+    const long long h = q0 * b.span1 + min(b1 + (b.pdims > 1 ? 1 : 0), b.span1 - 1);
+    need |= (l <= hi) && (h >= lo);
+  }
+  return need;
+}
+
+__global__ void shard_bounds_kernel(const double* __restrict__ x, int64_t n, int64_t ld, int pdims,
+                                    double eps, long long* mm) {
+  long long lo0 = LLONG_MAX, hi0 = LLONG_MIN, lo1 = LLONG_MAX, hi1 = LLONG_MIN;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const long long c0 = bin_coord(x[i * ld], eps);
+    lo0 = min(lo0, c0);
+    hi0 = max(hi0, c0);
+    if (pdims > 1) {
+      const long long c1 = bin_coord(x[i * ld + 1], eps);
+      lo1 = min(lo1, c1);
+      hi1 = max(hi1, c1);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo0 = min(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
+    hi0 = max(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+    lo1 = min(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
+    hi1 = max(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+  }
+  if (lane_id() == 0) {
+    atomicMin(&mm[0], lo0);
+    atomicMax(&mm[1], hi0);
+    atomicMin(&mm[2], lo1);
+    atomicMax(&mm[3], hi1);
+  }
+}
+
+__global__ void shard_bounds_init(long long* mm) {
+  mm[0] = LLONG_MAX;
+  mm[1] = LLONG_MIN;
+  mm[2] = LLONG_MAX;
+  mm[3] = LLONG_MIN;
+}
+
+// Per-bin point counts; a shared-memory histogram per block when the bins fit.
+__global__ void shard_hist_kernel(const double* __restrict__ x, int64_t n, int64_t ld, Bins b,
+                                  unsigned long long* __restrict__ hist, int smem_bins) {
+  extern __shared__ unsigned int s_hist[];
+  const long long nbins = b.span0 * b.span1;
+  const bool local = nbins <= smem_bins;
+  if (local)
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    long long b0, b1;
+    point_bins(x + i * ld, b, b0, b1);
+    const long long L = b0 * b.span1 + b1;
+    if (L < 0 || L >= nbins) continue;  // outside the agreed bounds: caller error, dropped
+    if (local) atomicAdd(&s_hist[L], 1u);
+    else atomicAdd(&hist[L], 1ull);
+  }
+  __syncthreads();
+  if (local)
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+      if (s_hist[i]) atomicAdd(&hist[i], (unsigned long long)s_hist[i]);
+}
+
+struct HaloPred {
+  const double* x;
+  int64_t ld;
+  Bins b;
+  long long lo, hi;
+  __device__ bool operator()(int64_t i) const {
+    long long b0, b1;
+    point_bins(x + i * ld, b, b0, b1);
+    return bin_needed(b0, b1, b, lo, hi);
+  }
+};
+
+struct HaloCount {
+  HaloPred p;
+  __device__ int64_t operator()(int64_t i) const { return p(i) ? 1 : 0; }
+};
+
+struct HaloWrite {
+  HaloPred p;
+  int d;
+  double* out;
+  int64_t ld_out;
+  uint32_t* gid;
+  int64_t gid_base;
+  __device__ void operator()(int64_t i, int64_t at) const {
+    if (!p(i)) return;
+    const double* src = p.x + i * p.ld;
+    double* dst = out + at * ld_out;
+    for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
+    gid[at] = uint32_t(gid_base + i);
+  }
+};
+
+struct NoStore {
+  __device__ void operator()(int64_t, int64_t) const {}
+};
+
+// First cell c of the local grid whose bin index is >= target (cells are
+// lexicographic, so their prefix bins are non-decreasing).
+__global__ void cell_bound_kernel(const double* __restrict__ P, const int64_t* __restrict__ cell_start,
+                                  int64_t n_cells, int d_pad, Bins b, long long lo, long long hi,
+                                  int64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int side = 0; side < 2; ++side) {
+    const long long target = side == 0 ? lo : hi + 1;
+    int64_t a = 0, z = n_cells;
+    while (a < z) {
+      const int64_t mid = (a + z) >> 1;
+      long long b0, b1;
+      point_bins(P + cell_start[mid] * d_pad, b, b0, b1);
+      if (b0 * b.span1 + b1 < target) a = mid + 1;
+      else z = mid;
+    }
+    out[side] = a;
+  }
+}
+
+__global__ void remap_ids_kernel(uint32_t* __restrict__ ids, int64_t m, const uint32_t* __restrict__ gid) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+       e += int64_t(gridDim.x) * blockDim.x)
+    ids[e] = gid[ids[e]];
+}
+
+__global__ void scatter_counts_kernel(const int64_t* __restrict__ loff, int64_t n_rows,
+                                      const uint32_t* __restrict__ gid, int32_t* __restrict__ counts) {
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < n_rows;
+       l += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = loff[l + 1] - loff[l];
+    if (c) counts[gid[l]] = int32_t(c);
+  }
+}
+
+// Warp per local row: copy the row (ids already global) to its global offset.
+__global__ void place_rows_kernel(const int64_t* __restrict__ loff, const uint32_t* __restrict__ nbr,
+                                  int64_t n_rows, const uint32_t* __restrict__ gid,
+                                  const int64_t* __restrict__ goff, uint32_t* __restrict__ dst) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t l = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; l < n_rows; l += warps) {
+    const int64_t a = loff[l], z = loff[l + 1];
+    if (a == z) continue;
+    uint32_t* out = dst + goff[gid[l]];
+    for (int64_t e = a + lane_id(); e < z; e += 32) out[e - a] = nbr[e];
+  }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), int64_t(kNumSMs) * 16)));
+}
+
+static Bins make_bins(int pdims, double eps, const int64_t* origin, const int64_t* span) {
+  Bins b;
+  b.pdims = pdims;
+  b.eps = eps;
+  b.origin0 = origin[0];
+  b.origin1 = pdims > 1 ? origin[1] : 0;
+  b.span0 = span[0];
+  b.span1 = pdims > 1 ? span[1] : 1;
+  return b;
+}
+
+void shard_bounds(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int pdims, double eps,
+                  int64_t* lo, int64_t* hi, cudaStream_t s) {
+  ctx->minmax.ensure(sizeof(long long) * (2 * TJ_MAX_K_IDX + 4), s);
+  long long* mm = ctx->minmax.as<long long>();
+  shard_bounds_init<<<1, 1, 0, s>>>(mm);
+  TJ_CHECK_LAUNCH();
+  if (n > 0) {
+    shard_bounds_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, pdims, eps, mm);
+    TJ_CHECK_LAUNCH();
+  }
+  long long h[4];
+  TJ_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  lo[0] = h[0];
+  hi[0] = h[1];
+  if (pdims > 1) {
+    lo[1] = h[2];
+    hi[1] = h[3];
+  }
+}
+
+void shard_histogram(const double* x, int64_t n, int64_t ld, int pdims, double eps,
+                     const int64_t* origin, const int64_t* span, int64_t* hist, cudaStream_t s) {
+  const Bins b = make_bins(pdims, eps, origin, span);
+  const int64_t nbins = b.span0 * b.span1;
+  TJ_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * nbins, s));
+  if (n == 0) return;
+  constexpr int kSmemBins = 12288;  // 48 KB of 32-bit counters
+  const size_t smem = nbins <= kSmemBins ? sizeof(unsigned) * size_t(nbins) : 0;
+  shard_hist_kernel<<<grid_for(n, 256), 256, smem, s>>>(
+      x, n, ld, b, reinterpret_cast<unsigned long long*>(hist), kSmemBins);
+  TJ_CHECK_LAUNCH();
+}
+
+int64_t shard_select(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int pdims,
+                     double eps, const int64_t* origin, const int64_t* span, int64_t own_lo,
+                     int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid, int64_t gid_base,
+                     int64_t capacity, cudaStream_t s) {
+  const Bins b = make_bins(pdims, eps, origin, span);
+  const HaloPred pred{x, ld, b, own_lo, own_hi};
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+  if (!out) {
+    scan_exclusive(HaloCount{pred}, NoStore{}, n, sc, s);
+  } else {
+    scan_exclusive(HaloCount{pred}, HaloWrite{pred, d, out, ld_out, gid, gid_base}, n, sc, s);
+  }
+  int64_t total = 0;
+  TJ_CUDA(cudaMemcpyAsync(&total, sc.total, sizeof(total), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  if (out && total > capacity) fail(TJ_ECAPACITY, "shard_select: output capacity too small");
+  return total;
+}
+
+void shard_cell_range(tj_ctx* ctx, int pdims, const int64_t* origin, const int64_t* span,
+                      int64_t own_lo, int64_t own_hi, int64_t* begin, int64_t* end, cudaStream_t s) {
+  const GridState& g = ctx->g;
+  const Bins b = make_bins(pdims, g.eps, origin, span);
+  ctx->tmp64.ensure(sizeof(int64_t) * std::max<int64_t>(g.n + 1, 2), s);
+  int64_t* out = ctx->tmp64.as<int64_t>();
+  cell_bound_kernel<<<1, 32, 0, s>>>(ctx->P.as<double>(), ctx->cell_start.as<int64_t>(), g.n_cells,
+                                     g.d_pad, b, own_lo, own_hi, out);
+  TJ_CHECK_LAUNCH();
+  int64_t h[2];
+  TJ_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TJ_CUDA(cudaStreamSynchronize(s));
+  *begin = h[0];
+  *end = h[1];
+}
+
+void shard_remap_ids(uint32_t* ids, int64_t m, const uint32_t* gid, cudaStream_t s) {
+  if (m <= 0) return;
+  remap_ids_kernel<<<grid_for(m, 256), 256, 0, s>>>(ids, m, gid);
+  TJ_CHECK_LAUNCH();
+}
+
+void shard_scatter_counts(const int64_t* loff, int64_t n_rows, const uint32_t* gid, int32_t* counts,
+                          cudaStream_t s) {
+  if (n_rows <= 0) return;
+  scatter_counts_kernel<<<grid_for(n_rows, 256), 256, 0, s>>>(loff, n_rows, gid, counts);
+  TJ_CHECK_LAUNCH();
+}
+
+void shard_place_rows(const int64_t* loff, const uint32_t* nbr, int64_t n_rows, const uint32_t* gid,
+                      const int64_t* goff, uint32_t* dst, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  place_rows_kernel<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(loff, nbr, n_rows, gid, goff, dst);
+  TJ_CHECK_LAUNCH();
+}
+
+void counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
+                       cudaStream_t s) {
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+  scan_exclusive(LoadAt<int32_t>{counts}, StoreAt<int64_t>{offsets}, n, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace tj

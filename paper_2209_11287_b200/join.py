@@ -244,10 +244,12 @@ _pinned: dict = {}
 
 
 def _pin(arr: np.ndarray) -> bool:
-    """Page-lock a host array once (cudaHostRegister) so H2D runs at full link speed.
+    """Page-lock a host array once so H2D runs at full link speed.
 
-    The registration lives as long as the array; it is dropped when the array is
-    garbage collected.  Returns False if registration is not possible.
+    Memory torch already page-locked (read_dataset(pinned=True)) is used as is.
+    Otherwise tj_host_register (cudaHostRegister; a failure leaves no stale CUDA
+    error behind) pins it for the array's lifetime.  Returns False when the
+    array stays pageable (small, non-contiguous, or registration refused).
     """
     import weakref
 
@@ -258,14 +260,17 @@ def _pin(arr: np.ndarray) -> bool:
         return True
     if not arr.flags.c_contiguous or arr.nbytes < (1 << 20):
         return False
-    cudart = torch.cuda.cudart()
-    if int(cudart.cudaHostRegister(key, arr.nbytes, 0)) != 0:
+    if torch.from_numpy(arr).is_pinned():
+        return True
+    try:
+        _native.host_register(key, arr.nbytes)
+    except (RuntimeError, ValidationError):
         return False
 
     def _unregister(ptr=key):
         _pinned.pop(ptr, None)
         try:
-            cudart.cudaHostUnregister(ptr)
+            _native.host_unregister(ptr)
         except Exception:
             pass
 
@@ -445,15 +450,18 @@ def self_join(dataset, config: JoinConfig, max_result_pairs: int | None = None) 
     dataset = as_dataset(dataset)
     _validate_config(config)
     job = DeviceJoin(dataset, config)
-    coords = upload(dataset, job.device)
-    if config.reorder_dims and dataset.n >= 2:  # join.py:163-164, on the device
-        coords = reorder_dims_on_device(job.ctx, coords, dataset)
-    job.build(coords)
-    t_indexed = time.perf_counter()
-    total = job.refine(max_result_pairs=max_result_pairs)
-    offsets, neighbors = job.finalize_fetch()
-    t_end = time.perf_counter()
-    stats = job.stats()
+    # one native context per device holds the grid and result buffers: joins on
+    # the same device from several host threads run one after another
+    with job.ctx.lock:
+        coords = upload(dataset, job.device)
+        if config.reorder_dims and dataset.n >= 2:  # join.py:163-164, on the device
+            coords = reorder_dims_on_device(job.ctx, coords, dataset)
+        job.build(coords)
+        t_indexed = time.perf_counter()
+        total = job.refine(max_result_pairs=max_result_pairs)
+        offsets, neighbors = job.finalize_fetch()
+        t_end = time.perf_counter()
+        stats = job.stats()
     stats.pairs_emitted = total
     stats.index_seconds = t_indexed - t_start
     stats.refine_seconds = t_end - t_indexed

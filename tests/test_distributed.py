@@ -70,9 +70,138 @@ def test_two_rank_gloo_join_equals_single_process():
     assert min(shares) > 0
 
 
+def _strong_worker(rank, world, port, eps, shm_path, out_q):
+    """The strong layout's host logic with numpy/oracle standing in for the CUDA kernels
+    (shard.cu restated in distributed.point_bins / halo_mask): row slices, all-reduced
+    bounds + bin histogram, equal-cost bin ranges, all-gather, halo select, the owned
+    cells' rows, global offsets from all-reduced counts, rows placed in one shared
+    host segment at their global offsets."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_11287_b200.distributed import (
+        halo_mask,
+        plan_bins,
+        point_bins,
+        row_slice,
+    )
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ds = generate(GenSpec("exponential", 6000, 3, seed=11))  # every rank reads its slice
+        n, pdims = ds.n, 2
+        a, b = row_slice(n, rank, world)
+        rows = ds.coords[a:b]
+        c = np.floor(rows[:, :pdims] / eps).astype(np.int64)
+        bounds = torch.tensor(np.concatenate([c.min(0), -c.max(0)]))
+        dist.all_reduce(bounds, op=dist.ReduceOp.MIN)
+        origin = bounds[:pdims].numpy()
+        span = -bounds[pdims:].numpy() - origin + 1
+        b0, b1 = point_bins(rows, eps, pdims, origin)
+        hist = torch.from_numpy(np.bincount(b0 * span[1] + b1, minlength=int(span[0] * span[1])))
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
+        plan = plan_bins(hist.numpy(), pdims, origin, span, world)
+        lo, hi = plan.owned(rank)
+        full = [torch.zeros((row_slice(n, 0, world)[1], rows.shape[1]), dtype=torch.float64)
+                for _ in range(world)]
+        mine = torch.zeros_like(full[0])
+        mine[: len(rows)] = torch.from_numpy(rows)
+        dist.all_gather(full, mine)
+        allx = torch.cat(full)[:n].numpy()
+        fb0, fb1 = point_bins(allx, eps, pdims, origin)
+        keep = halo_mask(fb0, fb1, span, pdims, lo, hi)
+        gid = np.flatnonzero(keep)  # stable: local ids monotone in global ids
+        local = np.ascontiguousarray(allx[keep])
+        _, cstart, ccoord, _ = oracle.grid(local, eps)
+        cell_bin = (ccoord[:, 0] - origin[0]) * span[1] + (ccoord[:, 1] - origin[1])
+        owned = np.flatnonzero((cell_bin >= lo) & (cell_bin <= hi))
+        assert np.all(np.diff(owned) == 1) or len(owned) <= 1  # one contiguous cell range
+        loff, lnb = oracle.join_csr(local, eps, cells=owned)
+        gnb = gid[lnb.astype(np.int64)]
+        counts = torch.zeros(n, dtype=torch.int64)
+        counts[gid] = torch.from_numpy(np.diff(loff))
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+        goff = np.concatenate([[0], np.cumsum(counts.numpy())])
+        if rank == 0:
+            np.zeros(int(goff[-1]), np.int64).tofile(shm_path)
+        dist.barrier()
+        out = np.memmap(shm_path, dtype=np.int64, mode="r+", shape=(int(goff[-1]),))
+        for l in np.flatnonzero(np.diff(loff)):  # rows straight to their global places
+            out[goff[gid[l]]: goff[gid[l] + 1]] = gnb[loff[l]: loff[l + 1]]
+        out.flush()
+        dist.barrier()
+        share = int(plan.cost_share()[rank])
+        out_q.put((rank, goff if rank == 0 else None,
+                   np.array(out) if rank == 0 else None, share, len(local), len(rows)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strong_layout_gloo_equals_single_process(world, tmp_path):
+    eps = 0.02
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    shm = str(tmp_path / "csr.bin")
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, eps, shm, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=180) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ds = generate(GenSpec("exponential", 6000, 3, seed=11))
+    full_off, full_nb = oracle.join_csr(ds, eps)
+    assert np.array_equal(results[0][1], full_off)
+    assert np.array_equal(results[0][2], full_nb.astype(np.int64))
+    shares = [r[3] for r in results]
+    assert min(shares) > 0  # every rank owns work (skewed 6000 points: coarse bins)
+    assert sum(r[4] for r in results) < world * ds.n  # ranks hold bins + halo, not all of it
+
+
+def test_plan_bins_balances_uniform_costs():
+    """c5's shape: 44 x 44 bins of ~equal density over 8 ranks -> shares within 2%."""
+    from paper_2209_11287_b200.distributed import plan_bins
+
+    rng = np.random.default_rng(1)
+    hist = rng.poisson(25_800, size=44 * 44)
+    plan = plan_bins(hist, 2, (0, 0), (44, 44), 8)
+    shares = np.array(plan.cost_share(), dtype=float)
+    assert shares.min() > 0.98 * shares.mean() and shares.max() < 1.02 * shares.mean()
+    lo = [r[0] for r in plan.ranges]
+    hi = [r[1] for r in plan.ranges]
+    assert lo[0] == 0 and hi[-1] == 44 * 44 - 1 and all(lo[i + 1] == hi[i] + 1 for i in range(7))
+
+
+def test_halo_mask_matches_definition():
+    """halo_mask (the numpy twin of shard.cu bin_needed) = 'some Chebyshev-1 neighbour
+    bin is owned', checked by enumeration."""
+    from paper_2209_11287_b200.distributed import halo_mask
+
+    rng = np.random.default_rng(5)
+    for pdims, span in ((2, (7, 5)), (1, (9, 1))):
+        b0 = rng.integers(0, span[0], 400)
+        b1 = rng.integers(0, span[1], 400)
+        for lo, hi in ((0, 0), (3, 17), (12, 12), (20, span[0] * span[1] - 1), (5, 4)):
+            got = halo_mask(b0, b1, span, pdims, lo, hi)
+            for i in range(len(b0)):
+                want = False
+                for a in (-1, 0, 1):
+                    for c in ((-1, 0, 1) if pdims > 1 else (0,)):
+                        q0, q1 = b0[i] + a, b1[i] + c
+                        if 0 <= q0 < span[0] and 0 <= q1 < span[1]:
+                            want |= lo <= q0 * span[1] + q1 <= hi
+                assert got[i] == want
+
+
 def _gpu_worker(rank, world, port, eps, kernel, out_q):
-    """The real multi-GPU path (shard_self_join: broadcast, cost-balanced tj_refine,
-    gather) with two ranks sharing cuda:0 over gloo (NCCL needs distinct GPUs)."""
+    """The real strong layout (strong_self_join: bin plan, all-gather, tj_shard_select,
+    tj_refine of the owned cells, global offsets, rows placed in the shared mapped host
+    CSR) with two ranks sharing cuda:0 over gloo (NCCL needs distinct GPUs)."""
     import torch
     import torch.distributed as dist
 
@@ -85,12 +214,12 @@ def _gpu_worker(rank, world, port, eps, kernel, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         ds = generate(GenSpec("uniform", 40_000, 4, seed=4)) if rank == 0 else None
-        (off, nb), merged, job = shard_self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, device=0))
-        own = int(job.total)
+        shard, merged = shard_self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, device=0))
+        info = (shard.pairs, shard.n_local, shard.total_pairs)
         if rank == 0:
-            out_q.put((merged[0], merged[1], own))
+            out_q.put((merged[0], merged[1], info))
         else:
-            out_q.put((None, None, own))
+            out_q.put((None, None, info))
     finally:
         dist.destroy_process_group()
 
@@ -115,7 +244,9 @@ def test_two_rank_shard_self_join_on_gpu(kernel):
     merged = [r for r in results if r[0] is not None][0]
     assert np.array_equal(merged[0], full_off)
     assert np.array_equal(np.asarray(merged[1], np.int64), full_nb.astype(np.int64))
-    assert all(r[2] > 0 for r in results) and sum(r[2] for r in results) == int(full_off[-1])
+    infos = [r[2] for r in results]
+    assert all(i[0] > 0 for i in infos) and sum(i[0] for i in infos) == int(full_off[-1])
+    assert all(i[1] < ds.n for i in infos)  # each rank holds its bins + halo, not everything
 
 
 def test_weak_scaling_partition_is_exact():
