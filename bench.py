@@ -466,12 +466,16 @@ def run_ours(args, world, rank, local):
         C = int(round(sum_over_ranks(float(weak_range["C"]), world)))
     value = 2.0 * d * C / (step_ms * 1e-3) / 1e12
 
-    # TC vs CUDA-core: the other kernel on the same harness
-    other = "scalar" if args.kernel == "tile" else "tile"
-    ocfg = JoinConfig(epsilon=eps, kernel=other, short_circuit=cfg.short_circuit, device=dev)
-    o_t, _, _ = measure(ocfg, max(1, min(args.steps, 3)), 1)
-    o_step = max_over_ranks(float(np.mean([t["step_ms"] for t in o_t])), world)
-    o_ref = max_over_ranks(float(np.mean([t["refine_kernel_ms"] for t in o_t])), world)
+    # TC vs CUDA-core: every other kernel on the same harness -- the reference's
+    # exact scalar order, the FMA direct form and the expanded form in DFMA
+    others = {}
+    for other in ("tile", "scalar", "core_fma", "core_expanded"):
+        if other == args.kernel:
+            continue
+        ocfg = JoinConfig(epsilon=eps, kernel=other, short_circuit=cfg.short_circuit, device=dev)
+        o_t, _, _ = measure(ocfg, max(1, min(args.steps, 3)), 1)
+        others[other] = (max_over_ranks(float(np.mean([t["step_ms"] for t in o_t])), world),
+                         max_over_ranks(float(np.mean([t["refine_kernel_ms"] for t in o_t])), world))
 
     # roofline of the dominant kernel (refine), FP64 peak measured in-run
     peak_dmma, _ = _native.fp64_peak(1)
@@ -555,9 +559,10 @@ def run_ours(args, world, rank, local):
                      "share_of_step": share},
         "secondary_rooflines": secondary_rooflines(n, d, dp, timings),
         "tc_vs_core": {args.kernel: {"step_ms": step_ms, "refine_kernel_ms": ref_ms,
-                                     "refine_tflops": achieved},
-                       other: {"step_ms": o_step, "refine_kernel_ms": o_ref,
-                               "refine_tflops": 2.0 * d * rank_c / (o_ref * 1e-3) / 1e12}},
+                                     "refine_tflops": achieved}} | {
+            k: {"step_ms": o_step, "refine_kernel_ms": o_ref,
+                "refine_tflops": 2.0 * d * rank_c / (o_ref * 1e-3) / 1e12}
+            for k, (o_step, o_ref) in others.items()},
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "seconds": e2e_s,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "self_join(host Dataset, JoinConfig) -> CSR in pinned host memory"
@@ -727,7 +732,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
                     help="workload (default: c2 on one GPU, c5 strong-scaled over N > 1)")
-    ap.add_argument("--kernel", choices=("tile", "scalar"), default="tile")
+    ap.add_argument("--kernel", choices=("tile", "scalar", "core_fma", "core_expanded"), default="tile")
     ap.add_argument("--no-short-circuit", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="strong",

@@ -36,6 +36,9 @@ extern "C" {
 
 #define TJ_KERNEL_CORE 0 /* CUDA-core FP64 direct form, GDS-Join style ("scalar") */
 #define TJ_KERNEL_DMMA 1 /* mma.sync m8n8k4 f64 expanded form, paper Alg. 2 ("tile") */
+/* CUDA-core comparison kernels (same pair set; values near eps^2 re-decided exactly): */
+#define TJ_KERNEL_CORE_FMA 2      /* direct form with fused multiply-add ("core_fma") */
+#define TJ_KERNEL_CORE_EXPANDED 3 /* expanded form |q|^2+|c|^2-2q.c in DFMA ("core_expanded") */
 
 /* Largest k_idx the device grid enumerates (3^(k-1) neighbour rows per cell). */
 #define TJ_MAX_K_IDX 8

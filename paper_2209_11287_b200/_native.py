@@ -18,7 +18,7 @@ from .errors import ResourceError, ValidationError
 LIB_PATH = Path(__file__).resolve().parent / "libtedjoin.so"
 
 TJ_OK, TJ_EINVAL, TJ_ECAPACITY, TJ_ECUDA, TJ_ENOMEM = 0, 1, 2, 3, 4
-TJ_KERNEL_CORE, TJ_KERNEL_DMMA = 0, 1
+TJ_KERNEL_CORE, TJ_KERNEL_DMMA, TJ_KERNEL_CORE_FMA, TJ_KERNEL_CORE_EXPANDED = 0, 1, 2, 3
 TJ_MAX_K_IDX = 8
 TJ_MAX_DIM = 128
 

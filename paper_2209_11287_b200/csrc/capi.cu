@@ -257,8 +257,8 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
     const GridState& g = ctx->g;
-    if (kernel != TJ_KERNEL_CORE && kernel != TJ_KERNEL_DMMA)
-      fail(TJ_EINVAL, "kernel must be TJ_KERNEL_CORE or TJ_KERNEL_DMMA");
+    if (kernel < TJ_KERNEL_CORE || kernel > TJ_KERNEL_CORE_EXPANDED)
+      fail(TJ_EINVAL, "kernel must be one of TJ_KERNEL_CORE, _DMMA, _CORE_FMA, _CORE_EXPANDED");
     if (cell_begin < 0 || cell_end > g.n_cells || cell_begin > cell_end)
       fail(TJ_EINVAL, "cell range out of bounds");
     ctx->have_refine_timing = false;
@@ -311,7 +311,13 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
     if (lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
     else if (dmma) launch_refine_tc(a, g.n, g.n_cells, s);
-    else launch_refine_core(a, s);
+    else {
+      // CUDA-core variants (refine_core.cu): the expanded form needs finite norms
+      const int variant = kernel == TJ_KERNEL_CORE_FMA                   ? 1
+                          : kernel == TJ_KERNEL_CORE_EXPANDED && norms_ok ? 2
+                                                                          : 0;
+      launch_refine_core(a, variant, s);
+    }
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;
     // low-d rows are counted from the hit masks (pairs per query + total hits)

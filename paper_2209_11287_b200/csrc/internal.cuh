@@ -150,7 +150,8 @@ int64_t build_work_items(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, int 
 ScanScratch scan_scratch(tj_ctx* ctx, int64_t n, cudaStream_t s);
 void build_mask_bases(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, cudaStream_t s);
 // refine_core.cu / refine_dmma.cu
-void launch_refine_core(const RefineArgs& a, cudaStream_t s);
+// variant: 0 exact reference order, 1 FMA direct form, 2 expanded form (refine_core.cu)
+void launch_refine_core(const RefineArgs& a, int variant, cudaStream_t s);
 void launch_refine_tc(const RefineArgs& a, int64_t n, int64_t n_cells,
                       cudaStream_t s);  // DMMA, 5 <= d <= 64
 void launch_refine_lowd(const RefineArgs& a, int64_t n, int64_t n_cells,

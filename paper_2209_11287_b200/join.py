@@ -40,7 +40,8 @@ class JoinConfig:
     """Join parameters (join.py:30-46); only epsilon affects which pairs are returned.
 
     kernel: 'tile' = DMMA tensor-core path, 'scalar' = CUDA-core FP64 path,
-        'auto' = the faster one for this d from measured throughput (extension).
+        'auto' = the faster one for this d from measured throughput (extension);
+        'core_fma' / 'core_expanded' = CUDA-core FMA direct / expanded form (extension).
     batch_size: target estimated pairs per batch (None = one batch).
     k_idx: indexed dimensions, default min(d, 6); the device grid supports <= 8.
     thread_count: accepted for compatibility (host threading has no role here).
@@ -201,9 +202,10 @@ def _validate_config(config: JoinConfig) -> None:
     """join.py:218-226."""
     if not np.isfinite(config.epsilon) or config.epsilon <= 0:
         raise ValidationError(f"epsilon must be positive and finite, got {config.epsilon}")
-    if config.kernel not in ("tile", "scalar", "auto"):
+    if config.kernel not in KERNEL_CODES and config.kernel != "auto":
         raise ValidationError(
-            f"kernel must be 'tile', 'scalar' or 'auto', got {config.kernel!r}")
+            f"kernel must be 'tile', 'scalar' or 'auto' (or {', '.join(CORE_VARIANTS)}), "
+            f"got {config.kernel!r}")
     if config.batch_size is not None and config.batch_size < 1:
         raise ValidationError(f"batch_size must be >= 1, got {config.batch_size}")
     if config.thread_count < 1:
@@ -227,6 +229,15 @@ def resolve_k_idx(config: JoinConfig, d: int) -> int:
 MEASURED_KERNEL_TFLOPS = ((2, 4.44, 1.39), (4, 9.44, 4.71), (8, 13.17, 6.38), (16, 16.78, 6.36),
                           (32, 19.09, 5.36))
 DMMA_MAX_DIM = 64
+
+# JoinConfig.kernel -> tj_refine kernel code.  'tile' and 'scalar' are the
+# reference's two kernels (join.py:34-41); the two extra CUDA-core variants do the
+# FMA direct form and the expanded form in DFMA (same pair set, for the
+# tensor-core vs CUDA-core comparison; refine_core.cu).
+CORE_VARIANTS = ("core_fma", "core_expanded")
+KERNEL_CODES = {"tile": _native.TJ_KERNEL_DMMA, "scalar": _native.TJ_KERNEL_CORE,
+                "core_fma": _native.TJ_KERNEL_CORE_FMA,
+                "core_expanded": _native.TJ_KERNEL_CORE_EXPANDED}
 
 
 def resolve_kernel(kernel: str, d: int) -> str:
@@ -304,8 +315,7 @@ class DeviceJoin:
         self.ctx = _native.context(device if device is not None else config.device)
         self.device = self.ctx.device
         self.kernel_name = resolve_kernel(config.kernel, work.d)
-        self.kernel = (_native.TJ_KERNEL_DMMA if self.kernel_name == "tile"
-                       else _native.TJ_KERNEL_CORE)
+        self.kernel = KERNEL_CODES[self.kernel_name]
         self.torch = torch
         self.coords = None
         self.info = None

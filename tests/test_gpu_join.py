@@ -27,6 +27,7 @@ from paper_2209_11287_b200 import grid as tgrid
 
 pytestmark = pytest.mark.gpu
 KERNELS = ("tile", "scalar")
+ALL_KERNELS = ("tile", "scalar", "core_fma", "core_expanded")  # + the CUDA-core comparison variants
 
 
 def assert_oracle_equal(res, ds, eps, k_idx=None):
@@ -191,7 +192,7 @@ def _sweep_cases():
 
 
 @pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{c['dist'][:3]}-n{c['n']}-d{c['d']}-S{c['target']}")
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", ALL_KERNELS)
 def test_spec_sweep_matches_reference(case, kernel):
     ds = generate(GenSpec(case["dist"], case["n"], case["d"], seed=case["seed"]))
     assert ds.checksum() == case["checksum"]
@@ -291,7 +292,7 @@ def test_grid_candidates_match_oracle():
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 7, 8, 9, 12, 16, 17, 24, 33, 64])
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", ALL_KERNELS)
 def test_dimensionality_ladder(d, kernel):
     ds = generate(GenSpec("uniform", 1500, d, seed=d))
     eps = 0.12 * math.sqrt(d)
@@ -416,3 +417,18 @@ def test_split_finalize_matches_one_call(d, kernel):
     assert np.array_equal(off_a, off_b) and np.array_equal(nbr_a, nbr_b)
     off, nb = oracle.join_csr(ds, eps)
     assert csr_equal(off_a, nbr_a, off, nb)
+
+
+@pytest.mark.parametrize("kernel", ALL_KERNELS)
+@pytest.mark.parametrize("d", [2, 3, 4, 8])
+def test_lattice_boundary_pairs(kernel, d):
+    """A lattice at spacing eps: every axis neighbour sits exactly on the boundary (in
+    exact arithmetic) and rounding decides -- the guard band / recheck path of every
+    non-exact kernel must reproduce the reference direct-form decisions."""
+    side = {2: 40, 3: 12, 4: 6, 8: 3}[d]
+    axes = np.meshgrid(*[np.arange(side) * 0.1 + 0.3] * d, indexing="ij")
+    pts = np.stack([a.reshape(-1) for a in axes], axis=1)
+    ds = Dataset(pts)
+    for eps in (0.1, 0.1 * math.sqrt(2), 0.2):
+        r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+        assert_oracle_equal(r, ds, eps)
