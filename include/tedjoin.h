@@ -129,6 +129,15 @@ int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream
 int tj_finalize_offsets(tj_ctx* ctx, int64_t* offsets, void* stream);
 int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, void* stream);
 
+/* The rows of the original ids [id_begin, id_end) only, into their CSR places
+ * (offsets from tj_finalize_offsets).  Once the stream reaches the end of this
+ * call the range's part of neighbors is final, so a caller can copy it to the
+ * host while the next range is built (the pinned, chunked result pipeline of
+ * DeviceJoin.finalize_fetch).  Low-d DMMA results are emitted straight by id;
+ * for other kernels the first call builds every row.  Asynchronous. */
+int tj_finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
+                           int64_t id_begin, int64_t id_end, void* stream);
+
 /* Counters accumulated since the last tj_reset_results (synchronous). */
 int tj_get_stats(tj_ctx* ctx, tj_stats* out);
 

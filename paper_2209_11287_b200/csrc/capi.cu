@@ -49,6 +49,7 @@ static void require_grid(tj_ctx* ctx) {
 
 static void zero_results(tj_ctx* ctx, cudaStream_t s) {
   ctx->ctr_valid = false;
+  ctx->rows_range_done = false;
   ctx->counters.ensure(sizeof(DevCounters), s);
   TJ_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(DevCounters), s));
   if (ctx->g.n > 0) {
@@ -126,7 +127,7 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
                     &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
                     &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
-                    &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX};
+                    &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -159,6 +160,7 @@ int tj_build_grid(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64
     if (!coords) fail(TJ_EINVAL, "coords is null");
     if (ld < d) fail(TJ_EINVAL, "ld must be >= d");
     ctx->masks_ready = false;
+    ctx->id_maps_ready = false;
     build_grid(ctx, coords, n, d, ld, k_idx, eps, s);
     zero_results(ctx, s);
     ctx->last_stream = s;
@@ -263,6 +265,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
       fail(TJ_EINVAL, "cell range out of bounds");
     ctx->have_refine_timing = false;
     ctx->ctr_valid = false;
+    ctx->rows_range_done = false;
     if (cell_begin == cell_end) return;
     // The expanded form needs finite norms; beyond that the exact kernel decides.
     const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
@@ -273,12 +276,17 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
       reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
     }
     if (lowd) ensure_masks(ctx, s);
-    const int qpi = lowd ? lowd_queries_per_item(g.n, g.n_cells)
+    // big cells at d_pad >= 12: the CTA-blocked Gram kernel (refine_gram.cu)
+    const bool gram = dmma && !lowd && gram_applies(g.d_pad, g.n, g.n_cells);
+    const int qpi = lowd   ? lowd_queries_per_item(g.n, g.n_cells)
+                    : gram ? kGramQueries
                     : dmma ? tc_queries_per_item(g.d_pad, g.n, g.n_cells)
                            : core_queries_per_item(g.d, g.d_pad);
-    // lowd: items never split a candidate list (each query row comes from one item)
-    const int64_t target = lowd ? (int64_t(1) << 60)
-                                : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
+    // lowd: items never split a candidate list (each query row comes from one item);
+    // gram: 64-query items x 32k-candidate slices
+    const int64_t target = lowd   ? (int64_t(1) << 60)
+                           : gram ? int64_t(kGramQueries) * kGramSlice
+                                  : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
     ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s,
                                     lowd ? &counters(ctx)->n_items : nullptr);
     TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
@@ -310,6 +318,7 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     a.short_circuit = short_circuit ? 1 : 0;
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
     if (lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
+    else if (gram) launch_refine_gram(a, s);
     else if (dmma) launch_refine_tc(a, g.n, g.n_cells, s);
     else {
       // CUDA-core variants (refine_core.cu): the expanded form needs finite norms
@@ -402,6 +411,30 @@ int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, v
   if (!ctx || !offsets) return TJ_EINVAL;
   return guarded(ctx, [&] {
     finalize_phase(ctx, const_cast<int64_t*>(offsets), neighbors, stream, 2);
+  });
+}
+
+int tj_finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
+                           int64_t id_begin, int64_t id_end, void* stream) {
+  if (!ctx || !offsets) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    if (id_begin < 0 || id_end > ctx->g.n || id_begin > id_end) fail(TJ_EINVAL, "id range out of bounds");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    DevCounters c = ctx->ctr;
+    if (!ctx->ctr_valid) {
+      TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, s));
+      TJ_CUDA(cudaStreamSynchronize(s));
+      ctx->ctr = c;
+      ctx->ctr_valid = true;
+    }
+    if (c.pairs > ctx->pair_cap)
+      fail(TJ_ECAPACITY, "result buffer overflowed; call tj_result_count and re-run the batch");
+    if (c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
+    if (c.pairs + c.hits == 0) return;
+    finalize_rows_range(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits),
+                        int64_t(c.max_row), id_begin, id_end, s);
   });
 }
 

@@ -126,6 +126,9 @@ struct tj_ctx {
   // results
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
+  tj::DevBuf ipos, pcell;        // id -> position, position -> cell (id-ordered emit)
+  bool id_maps_ready = false;    // ipos / pcell built for the current grid
+  bool rows_range_done = false;  // pair-path rows built by an earlier range call
   unsigned long long pair_cap = 0;
   int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
   int64_t n_items = 0;
@@ -157,6 +160,11 @@ void launch_refine_tc(const RefineArgs& a, int64_t n, int64_t n_cells,
 void launch_refine_lowd(const RefineArgs& a, int64_t n, int64_t n_cells,
                         cudaStream_t s);  // d <= 4, unsliced items
 int lowd_queries_per_item(int64_t n, int64_t n_cells);
+// refine_gram.cu: CTA-blocked DMMA for big cells at d_pad >= 12
+constexpr int kGramQueries = 64;
+constexpr int64_t kGramSlice = 32768;
+bool gram_applies(int d_pad, int64_t n, int64_t n_cells);
+void launch_refine_gram(const RefineArgs& a, cudaStream_t s);
 int core_queries_per_item(int d, int d_pad);
 int tc_queries_per_item(int d_pad, int64_t n, int64_t n_cells);
 // finalize.cu
@@ -196,4 +204,7 @@ void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* 
                        unsigned long long* max_row, cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
                   int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s, int phase = 3);
+void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
+                         int64_t n_mask_hits, int64_t max_mask_row, int64_t id_begin,
+                         int64_t id_end, cudaStream_t s);
 }  // namespace tj

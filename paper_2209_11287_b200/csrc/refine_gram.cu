@@ -1,0 +1,298 @@
+// DMMA refine for big cells at d >= 12 (d_pad >= 12): the brute-force regime of
+// config 4 d = 16 / 32 / 64 (64 cells or one cell, every pair a candidate).
+//
+// Reference: _TileRefiner / distance_tile_v2 (join.py:238-283, kernels.py:184-263):
+// D = (-2Q) * C^T + |c|^2 accumulated chunk by chunk, + |q|^2, emit <= eps^2.
+//
+// There the join is a dense Gram computation, and what limits the per-warp
+// kernel (refine_tc.cu: 16 queries per item, each staged candidate used by two
+// query groups) is operand traffic, not the DMMA pipe.  This kernel is blocked
+// like a GEMM:
+//  * a CTA (4 warps) owns a work item of <= 64 queries of one cell x a slice of
+//    its concatenated candidate list and sweeps the slice in 64-candidate stages;
+//  * the item's queries are staged once, scaled by -2, in shared memory; every
+//    stage's candidates arrive through a 2-deep cp.async ring (positions mapped
+//    from the cell's runs once per stage); rows are padded to a conflict-free
+//    stride and carry |c|^2 as the accumulator's start value;
+//  * warp w computes a 32 x 32 block (4 candidate blocks x 4 query groups = 16
+//    independent DMMA accumulator chains): per 4-dim chunk 4 A + 4 B fragment
+//    loads feed 16 DMMAs, so each staged candidate is used by 64 queries;
+//  * epilogue as refine_tc.cu: one branch per stage on the OR of the compare
+//    ballots; tiles with a passing value are handled one by one, guard-band
+//    values re-decided by the reference direct form, pairs through a per-warp
+//    shared-memory buffer;
+//  * no short-circuit: at these sizes every chunk is executed (chunks_skipped
+//    stays 0, chunks_executed = tiles * NCH in the reference's tiling).
+#include "internal.cuh"
+#include "refine_common.cuh"
+
+namespace tj {
+
+constexpr int kGramWarps = 4;
+constexpr int kGramThreads = kGramWarps * kWarp;
+constexpr int kGramQ = 64;   // queries per item
+constexpr int kGramC = 64;   // candidates per stage
+constexpr int kGramStages = 2;
+
+template <int NCH>
+struct GramShape {
+  static constexpr int DP = 4 * NCH;
+  static constexpr int STRIDE = (DP % 8 == 0) ? DP + 4 : DP;  // conflict-free fragment rows
+  static constexpr int PPR = DP / 2;                           // 16-byte pieces per row
+};
+
+template <int NCH>
+struct GramSmem {
+  using S = GramShape<NCH>;
+  double q[kGramQ][S::STRIDE];                   // -2 * query coordinates
+  double c[kGramStages][kGramC][S::STRIDE];      // candidate coordinates
+  double cn[kGramStages][kGramC];                // |c|^2 (padding rows: kPadNorm)
+  uint32_t pos[kGramStages][kGramC];             // cell-ordered positions
+  uint2 hits[kGramWarps][kHitBuf];
+};
+
+__device__ __forceinline__ void gram_cp16(void* smem, const void* gmem) {
+  const unsigned s = unsigned(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void gram_cp8(void* smem, const void* gmem) {
+  const unsigned s = unsigned(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void gram_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void gram_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// m8n8k4 f64 without `volatile`, so the scheduler may interleave the chains.
+__device__ __forceinline__ void gram_mma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __noinline__ uint2 gram_recheck(const double* P, int dp, int d, double eps_sq, bool b0,
+                                           bool b1, unsigned m0, unsigned m1, uint32_t qa,
+                                           uint32_t c, unsigned long long* ctr) {
+  bool p0 = (m0 >> lane_id()) & 1u, p1 = (m1 >> lane_id()) & 1u;
+  if (b0) p0 = direct_form_le(P, dp, d, qa, c, eps_sq);
+  if (b1) p1 = direct_form_le(P, dp, d, qa + 1, c, eps_sq);
+  const unsigned nb = __popc(__ballot_sync(0xffffffffu, b0)) + __popc(__ballot_sync(0xffffffffu, b1));
+  if (lane_id() == 0) atomicAdd(ctr, (unsigned long long)nb);
+  return make_uint2(__ballot_sync(0xffffffffu, p0), __ballot_sync(0xffffffffu, p1));
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs a) {
+  using S = GramShape<NCH>;
+  constexpr int DP = S::DP, PPR = S::PPR;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GramSmem<NCH>& sm = *reinterpret_cast<GramSmem<NCH>*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int row = lane >> 2, col = lane & 3;
+  const unsigned lt = lanemask_lt();
+  const int wc = warp & 1, wq = warp >> 1;  // the warp's 32 x 32 block of the 64 x 64 stage
+  uint2* hits = sm.hits[warp];
+  HitBuffer hb;
+  const double eps_sq = a.eps_sq;
+  unsigned long long st_tiles_ref = 0;
+  __shared__ unsigned long long s_item;
+
+  for (;;) {
+    __syncthreads();  // previous item's buffers are free
+    if (threadIdx.x == 0) s_item = atomicAdd(&a.ctr->item_next, 1ull);
+    __syncthreads();
+    const unsigned long long idx = s_item;
+    if (idx >= (unsigned long long)a.n_items) break;
+    const WorkItem it = a.items[idx];
+    const int nq = int(it.nq);
+    const int64_t rb = a.cell_runs[it.cell];
+    const int nr = int(a.cell_runs[it.cell + 1] - rb);
+    const uint32_t s0 = it.s0, s1 = it.s1;
+    const int nst = int((s1 - s0 + kGramC - 1) / kGramC);
+
+    // queries, scaled by -2 (exact), rows >= nq zero
+    for (int i = threadIdx.x; i < kGramQ * PPR; i += kGramThreads) {
+      const int r = i / PPR, pc = i - r * PPR;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < nq) v = *reinterpret_cast<const double2*>(a.P + size_t(it.q0 + r) * DP + 2 * pc);
+      sm.q[r][2 * pc] = -2.0 * v.x;
+      sm.q[r][2 * pc + 1] = -2.0 * v.y;
+    }
+    // thresholds of this lane's 8 queries: 8*(4*wq + g) + 2*col + jj
+    double thr[4][2], tlo[4][2];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int q = 32 * wq + 8 * g + 2 * col + jj;
+        const bool v = q < nq;
+        const double qn = v ? a.NRM[it.q0 + q] : 0.0;
+        const double guard = a.guard_rel * (qn + a.max_norm) + 1e-300;
+        thr[g][jj] = v ? eps_sq - qn + guard : -INFINITY;
+        tlo[g][jj] = v ? eps_sq - qn - guard : INFINITY;
+      }
+    unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    if (threadIdx.x == 0) st_tiles_ref += uint64_t((nq + 7) >> 3) * ((s1 - s0 + 7) >> 3);
+
+    // stage st: candidates s0 + 64 st + r; threads 0..63 map offsets to positions
+    auto issue = [&](int st) {
+      const int buf = st % kGramStages;
+      if (st < nst) {
+        if (threadIdx.x < kGramC) {
+          const uint32_t t = s0 + uint32_t(st) * kGramC + threadIdx.x;
+          uint32_t p = 0xffffffffu;
+          if (t < s1) {
+            int lo = 0, hi = nr;
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (a.run_off[rb + mid] <= t) lo = mid;
+              else hi = mid;
+            }
+            p = a.runs[rb + lo].x + (t - a.run_off[rb + lo]);
+          }
+          sm.pos[buf][threadIdx.x] = p;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kGramC * PPR; i += kGramThreads) {
+          const int r = i / PPR, pc = i - r * PPR;
+          const uint32_t p = sm.pos[buf][r];
+          if (p != 0xffffffffu) gram_cp16(&sm.c[buf][r][2 * pc], a.P + size_t(p) * DP + 2 * pc);
+          else *reinterpret_cast<double2*>(&sm.c[buf][r][2 * pc]) = make_double2(0.0, 0.0);
+        }
+        if (threadIdx.x < kGramC) {
+          const uint32_t p = sm.pos[buf][threadIdx.x];
+          if (p != 0xffffffffu) gram_cp8(&sm.cn[buf][threadIdx.x], a.NRM + p);
+          else sm.cn[buf][threadIdx.x] = kPadNorm;
+        }
+      }
+      gram_commit();
+    };
+    issue(0);
+#pragma unroll 1
+    for (int st = 0; st < nst; ++st) {
+      issue(st + 1);
+      gram_wait<1>();
+      __syncthreads();
+      const int buf = st % kGramStages;
+      double acc[4][4][2];  // [candidate block][query group][value]
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double cn = sm.cn[buf][32 * wc + 8 * b + row];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) acc[b][g][0] = acc[b][g][1] = cn;
+      }
+#pragma unroll 4
+      for (int j = 0; j < NCH; ++j) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) av[b] = sm.c[buf][32 * wc + 8 * b + row][4 * j + col];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) bv[g] = sm.q[32 * wq + 8 * g + row][4 * j + col];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int g = 0; g < 4; ++g) gram_mma(acc[b][g][0], acc[b][g][1], av[b], bv[g]);
+      }
+      // epilogue: one branch per stage
+      unsigned any = 0u;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          any |= __ballot_sync(0xffffffffu, acc[b][g][0] <= thr[g][0]) |
+                 __ballot_sync(0xffffffffu, acc[b][g][1] <= thr[g][1]);
+      if (any) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t cpos = sm.pos[buf][32 * wc + 8 * b + row];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const bool p0 = acc[b][g][0] <= thr[g][0];
+            const bool p1 = acc[b][g][1] <= thr[g][1];
+            unsigned m0 = __ballot_sync(0xffffffffu, p0);
+            unsigned m1 = __ballot_sync(0xffffffffu, p1);
+            if ((m0 | m1) == 0) continue;
+            const uint32_t qa = it.q0 + 32 * wq + 8 * g + 2 * col;
+            const bool b0 = p0 && acc[b][g][0] > tlo[g][0];
+            const bool b1 = p1 && acc[b][g][1] > tlo[g][1];
+            if (__any_sync(0xffffffffu, b0 || b1)) {
+              const uint2 m = gram_recheck(a.P, DP, a.d, eps_sq, b0, b1, m0, m1, qa, cpos,
+                                           &a.ctr->rechecks);
+              m0 = m.x;
+              m1 = m.y;
+              if ((m0 | m1) == 0) continue;
+            }
+            const bool h0 = (m0 >> lane) & 1u, h1 = (m1 >> lane) & 1u;
+            const int n0 = __popc(m0), n1 = __popc(m1);
+            hb.reserve(n0 + n1, hits, a);
+            if (h0) hits[hb.count + __popc(m0 & lt)] = make_uint2(qa, cpos);
+            if (h1) hits[hb.count + n0 + __popc(m1 & lt)] = make_uint2(qa + 1, cpos);
+            hb.count += n0 + n1;
+            qc[g][0] += h0;
+            qc[g][1] += h1;
+          }
+        }
+      }
+      __syncthreads();  // stage buffer `buf` is refilled by issue(st + 2)
+    }
+    gram_wait<0>();
+    // per-query counts (items of one cell share queries across slices: atomics)
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        unsigned c = qc[g][jj];
+        c += __shfl_xor_sync(0xffffffffu, c, 4);
+        c += __shfl_xor_sync(0xffffffffu, c, 8);
+        c += __shfl_xor_sync(0xffffffffu, c, 16);
+        const int q = 32 * wq + 8 * g + 2 * col + jj;
+        if (row == 0 && q < nq && c) atomicAdd(&a.qcount[it.q0 + q], c);
+      }
+    if (threadIdx.x == 0) atomicAdd(&a.ctr->refined, (unsigned long long)nq * (s1 - s0));
+  }
+  hb.flush(hits, a);
+  flush_stats(a, st_tiles_ref, st_tiles_ref * NCH, 0, 0);
+}
+
+// Items of <= 64 queries x candidate slices of ~32k (a multiple of 64).
+bool gram_applies(int d_pad, int64_t n, int64_t n_cells) {
+  return d_pad >= 12 && n >= int64_t(256) * n_cells;
+}
+
+template <int NCH>
+static void launch_gram_t(const RefineArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(GramSmem<NCH>);
+  auto kern = refine_gram_kernel<NCH>;
+  TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGramThreads, smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t grid = std::min<int64_t>(a.n_items, int64_t(kNumSMs) * per_sm);
+  kern<<<unsigned(std::max<int64_t>(grid, 1)), kGramThreads, smem, s>>>(a);
+  TJ_CHECK_LAUNCH();
+}
+
+void launch_refine_gram(const RefineArgs& a, cudaStream_t s) {
+  switch (a.nchunks) {
+    case 3: return launch_gram_t<3>(a, s);
+    case 4: return launch_gram_t<4>(a, s);
+    case 5: return launch_gram_t<5>(a, s);
+    case 6: return launch_gram_t<6>(a, s);
+    case 7: return launch_gram_t<7>(a, s);
+    case 8: return launch_gram_t<8>(a, s);
+    case 9: return launch_gram_t<9>(a, s);
+    case 10: return launch_gram_t<10>(a, s);
+    case 11: return launch_gram_t<11>(a, s);
+    case 12: return launch_gram_t<12>(a, s);
+    case 13: return launch_gram_t<13>(a, s);
+    case 14: return launch_gram_t<14>(a, s);
+    case 15: return launch_gram_t<15>(a, s);
+    case 16: return launch_gram_t<16>(a, s);
+    default: break;
+  }
+  fail(TJ_EINVAL, "Gram DMMA refine is instantiated for 9 <= d <= 64, got d=" + std::to_string(a.d));
+}
+
+}  // namespace tj

@@ -382,9 +382,16 @@ class DeviceJoin:
         torch.cuda.current_stream(self.device).synchronize()
         return off.numpy(), nbr.numpy()
 
-    def finalize_fetch(self):
-        """finalize() + fetch() with the offsets' D2H (side stream) overlapping the
-        row kernels; returns numpy (offsets, neighbors)."""
+    def finalize_fetch(self, chunks: int = 8):
+        """finalize() + fetch() as a pipeline into pinned host memory; returns numpy
+        (offsets, neighbors).
+
+        The offsets go first (their D2H on the copy stream overlaps the first rows).
+        The rows are then built in `chunks` ranges of original ids
+        (tj_finalize_rows_range): each range is one contiguous part of the CSR, final
+        when its kernels end, and its D2H on the copy stream overlaps the next range's
+        emit -- the double-buffered result pipeline of the north star, with the PCIe
+        copy engine running while the SMs emit."""
         torch = self.torch
         n = self.work.n
         dev = f"cuda:{self.device}"
@@ -392,19 +399,32 @@ class DeviceJoin:
         self.offsets_d = torch.empty(n + 1, dtype=torch.int64, device=dev)
         self.neighbors_d = torch.empty(max(self.total, 1), dtype=torch.int32, device=dev)
         off = torch.empty((n + 1,), dtype=torch.int64, pin_memory=True)
-        nbr = torch.empty((self.total,), dtype=torch.int32, pin_memory=True)
-        self.ctx.finalize_offsets(self.offsets_d)
+        nbr = torch.empty((max(self.total, 1),), dtype=torch.int32, pin_memory=True)
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream(device=self.device)
         cs = self._copy_stream
+        self.ctx.finalize_offsets(self.offsets_d)
         cs.wait_stream(main)
         with torch.cuda.stream(cs):
             off.copy_(self.offsets_d, non_blocking=True)
-        self.ctx.finalize_rows(self.offsets_d, self.neighbors_d)
-        nbr.copy_(self.neighbors_d[: self.total], non_blocking=True)
-        main.synchronize()
+            off_ready = torch.cuda.Event()
+            off_ready.record(cs)
+        bounds = [n * k // chunks for k in range(chunks + 1)]
+        for k in range(chunks):
+            a, b = bounds[k], bounds[k + 1]
+            self.ctx.finalize_rows_range(self.offsets_d, self.neighbors_d, a, b)
+            done = torch.cuda.Event()
+            done.record(main)
+            if k == 0:
+                off_ready.synchronize()  # host needs the offsets to size the copies
+            lo, hi = int(off[a]), int(off[b])
+            if hi > lo:
+                cs.wait_event(done)
+                with torch.cuda.stream(cs):
+                    nbr[lo:hi].copy_(self.neighbors_d[lo:hi], non_blocking=True)
         cs.synchronize()
-        return off.numpy(), nbr.numpy()
+        main.synchronize()
+        return off.numpy(), nbr[: self.total].numpy()
 
     def stats(self) -> JoinStats:
         st = self.ctx.stats()
