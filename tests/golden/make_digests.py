@@ -9,14 +9,18 @@ the FULL inputs of configs 1, 2, 3, 4 (d = 2, 4, 8) and 5 and records the
 order-independent digest of each pair set (count, two 64-bit sums of
 splitmix64(q << 32 | c); tests/digest.py), so the GPU suite can check the whole
 pair set at full size without a multi-GB fixture.  Configs 4 d >= 16 are
-brute force over 4e12 candidate pairs -- beyond this container's 8 cores; their
-full-size check is the GPU's exact direct-form brute force (tj_brute_force),
-itself pinned to the oracle at small n, plus the reference's sampled rows.
+brute force over 4e12 candidate pairs (hours of this container's 8 cores, the
+early exit of the running sum helps); they are also checked against the GPU's
+exact direct-form brute force (tj_brute_force, bf_digests.json), itself pinned
+to the oracle at full size on config 2.
+
+    TJ_ORACLE_THREADS=6 python tests/golden/make_digests.py c4d16 c4d32 c4d64
 """
 
 from __future__ import annotations
 
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -35,6 +39,10 @@ CONFIGS = {
     "c5": ("uniform", 50_000_000, 4, 0.0232204),
     "c4d8": ("uniform", 2_000_000, 8, 0.244686),
     "c3": ("exponential", 5_000_000, 8, 0.0118508),
+    # brute force over 4e12 candidate pairs: hours on 8 cores, run in the background
+    "c4d16": ("uniform", 2_000_000, 16, 0.657508),
+    "c4d32": ("uniform", 2_000_000, 32, 1.31923),
+    "c4d64": ("uniform", 2_000_000, 64, 2.27218),
 }
 
 
@@ -45,7 +53,7 @@ def main(names):
         dist, n, d, eps = CONFIGS[name]
         ds = generate(GenSpec(dist, n, d, seed=0))
         t = time.perf_counter()
-        dg = oracle.digest(ds, eps)
+        dg = oracle.digest(ds, eps, threads=int(os.environ.get("TJ_ORACLE_THREADS", "0")))
         dg.update({"dist": dist, "n": n, "d": d, "eps": eps, "checksum": ds.checksum(),
                    "oracle_seconds": round(time.perf_counter() - t, 1),
                    "oracle_threads": oracle.num_threads()})

@@ -432,3 +432,25 @@ def test_lattice_boundary_pairs(kernel, d):
     for eps in (0.1, 0.1 * math.sqrt(2), 0.2):
         r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
         assert_oracle_equal(r, ds, eps)
+
+
+@pytest.mark.parametrize("n,d,k_idx,eps", [
+    (3000, 12, 1, 0.788),    # 2 cells of ~1500: Gram items with partial query blocks
+    (2500, 16, 2, 0.55),     # 4 cells, ~1 neighbour per point
+    (2500, 16, 1, 1.051),    # one cell, ~29 neighbours per point
+    (1700, 33, 1, 1.792),    # one cell, d_pad = 36
+    (1300, 64, 1, 2.759),    # one cell, NCH = 16
+    (40000, 12, 1, 0.609),   # > one 32k-candidate slice per item
+])
+def test_gram_kernel_big_cells(n, d, k_idx, eps):
+    """Big cells at d_pad >= 12 take the CTA-blocked Gram DMMA kernel (refine_gram.cu):
+    its pair set, tile count and candidate count equal the oracle's / the reference formula."""
+    ds = generate(GenSpec("uniform", n, d, seed=n + d))
+    r = self_join(ds, JoinConfig(epsilon=eps, k_idx=k_idx))
+    assert_oracle_equal(r, ds, eps, k_idx=k_idx)
+    _, cstart, _, cand = oracle.grid(ds, eps, k_idx)
+    nq = np.diff(cstart)
+    assert r.stats.candidates_refined == int(np.sum(nq * cand))
+    tiles = int(np.sum(-(-nq // 8) * -(-cand // 8)))
+    assert r.stats.tiles_processed == tiles
+    assert r.stats.chunks_executed + r.stats.chunks_skipped == tiles * ((d + 3) // 4)

@@ -164,7 +164,7 @@ def test_gpu_brute_force_equals_oracle():
     for spec, eps in [(GenSpec("uniform", 1500, 3, seed=1), 0.08),
                       (GenSpec("exponential", 1200, 9, seed=2), 0.02)]:
         ds = generate(spec)
-        bf = brute_force_join(ds, eps)
+        bf = brute_force_join(ds, eps, force=True)
         assert np.array_equal(bf.pairs, oracle.brute_force(ds, eps))
 
 
@@ -175,7 +175,7 @@ def test_gpu_brute_force_equals_join_config1():
 
     ds = generate(GenSpec("uniform", 100_000, 2, seed=0))
     eps = 0.0143667
-    bf = brute_force_join(ds, eps)
+    bf = brute_force_join(ds, eps, force=True)
     r = self_join(ds, JoinConfig(epsilon=eps))
     assert csr_equal(bf.offsets, bf.neighbors, r.offsets, r.neighbors)
 
