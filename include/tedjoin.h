@@ -108,13 +108,21 @@ int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int6
  * ctx result buffer.  Asynchronous. */
 int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
               int64_t cell_end, void* stream);
-/* Pairs appended since the last tj_reset_results (synchronous).  If the append
- * buffer overflowed the ctx grows it and the caller must re-run the batch:
- * *overflowed is set to 1 and the buffer is left reset. */
+/* Result pairs since the last tj_reset_results (synchronous).  The count is exact
+ * even past the append buffer's capacity (CUDA-core and high-d DMMA kernels
+ * append pairs; the low-d DMMA kernel records hit masks and never overflows);
+ * *overflowed = 1 when appends were dropped -- the caller then rolls the batch
+ * back (tj_rollback_results), grows the buffer (tj_reserve_results) and re-runs it
+ * (the output-budget batcher of DeviceJoin.refine, join.py:184-202). */
 int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed);
 int tj_reset_results(tj_ctx* ctx, void* stream);
-/* Reserve append capacity for `pairs` result pairs (optional; the ctx sizes it itself). */
+/* Grow the pair append buffer to `pairs` entries, keeping what was appended so far. */
 int tj_reserve_results(tj_ctx* ctx, int64_t pairs);
+/* Snapshot the result counters (stream-ordered) before a batch ... */
+int tj_checkpoint_results(tj_ctx* ctx, void* stream);
+/* ... and undo that batch: counters back to the snapshot, the per-query counts of
+ * the cells [cell_begin, cell_end) zeroed.  Asynchronous. */
+int tj_rollback_results(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, void* stream);
 
 /* Canonical output (replaces the concat + lexsort of join.py:203-204): CSR by
  * original query id with neighbour ids ascending.  offsets: device int64[n+1];

@@ -53,6 +53,8 @@ SIGNATURES = {
     "tj_result_count": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
     "tj_reset_results": (_i32, [_vp, _vp]),
     "tj_reserve_results": (_i32, [_vp, _i64]),
+    "tj_checkpoint_results": (_i32, [_vp, _vp]),
+    "tj_rollback_results": (_i32, [_vp, _i64, _i64, _vp]),
     "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_finalize_offsets": (_i32, [_vp, _vp, _vp]),
     "tj_finalize_rows": (_i32, [_vp, _vp, _vp, _vp]),
@@ -194,6 +196,15 @@ class Context:
 
     def reserve_results(self, pairs: int):
         self._check(self.lib.tj_reserve_results(self.handle, int(pairs)))
+
+    def checkpoint_results(self, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_checkpoint_results(self.handle, s.cuda_stream))
+
+    def rollback_results(self, cell_begin: int, cell_end: int, stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_rollback_results(self.handle, int(cell_begin), int(cell_end),
+                                                 s.cuda_stream))
 
     def result_count(self):
         total, over = _i64(), _i32()

@@ -50,8 +50,8 @@ static void require_grid(tj_ctx* ctx) {
 static void zero_results(tj_ctx* ctx, cudaStream_t s) {
   ctx->ctr_valid = false;
   ctx->rows_range_done = false;
-  ctx->counters.ensure(sizeof(DevCounters), s);
-  TJ_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(DevCounters), s));
+  ctx->counters.ensure(2 * sizeof(DevCounters), s);  // live counters + a checkpoint
+  TJ_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 2 * sizeof(DevCounters), s));
   if (ctx->g.n > 0) {
     ctx->qcount.ensure(sizeof(uint32_t) * ctx->g.n, s);
     TJ_CUDA(cudaMemsetAsync(ctx->qcount.ptr, 0, sizeof(uint32_t) * ctx->g.n, s));
@@ -67,19 +67,29 @@ static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
   ctx->masks_ready = true;
 }
 
-static unsigned long long free_budget(double frac, size_t unit) {
-  size_t free_b = 0, total_b = 0;
-  TJ_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  return (unsigned long long)(frac * double(free_b)) / unit;
-}
 
-static void reserve_pairs(tj_ctx* ctx, unsigned long long pairs, cudaStream_t s) {
+// Grow the pair append buffer to `pairs` entries, keeping the first `keep`.
+static void reserve_pairs(tj_ctx* ctx, unsigned long long pairs, unsigned long long keep,
+                          cudaStream_t s) {
   pairs = std::max<unsigned long long>(pairs, 1024);
   if (pairs <= ctx->pair_cap) return;
+  keep = std::min(keep, ctx->pair_cap);
+  DevBuf grown;
+  grown.ensure(sizeof(uint2) * pairs, s);
+  if (keep) TJ_CUDA(cudaMemcpyAsync(grown.ptr, ctx->pairs.ptr, sizeof(uint2) * keep,
+                                    cudaMemcpyDeviceToDevice, s));
   ctx->pairs.release(s);
-  ctx->pair_cap = 0;
-  ctx->pairs.ensure(sizeof(uint2) * pairs, s);
+  ctx->pairs = grown;
+  grown.ptr = nullptr;
   ctx->pair_cap = pairs;
+}
+
+__global__ void zero_query_counts_kernel(const int64_t* __restrict__ cell_start, int64_t cb,
+                                         int64_t ce, uint32_t* __restrict__ qcount) {
+  const int64_t a = cell_start[cb], b = cell_start[ce];
+  for (int64_t p = a + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < b;
+       p += int64_t(gridDim.x) * blockDim.x)
+    qcount[p] = 0;
 }
 
 // Guard-band half-width relative to |q|^2 + max|c|^2 (+eps^2); see refine_dmma.cu.
@@ -248,7 +258,45 @@ int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int6
 
 int tj_reserve_results(tj_ctx* ctx, int64_t pairs) {
   if (!ctx || pairs < 0) return TJ_EINVAL;
-  return guarded(ctx, [&] { reserve_pairs(ctx, (unsigned long long)pairs, ctx->last_stream); });
+  return guarded(ctx, [&] {
+    // keep what was appended so far (the batches before an overflowing one)
+    DevCounters c{};
+    if (ctx->counters.ptr) {
+      TJ_CUDA(cudaMemcpyAsync(&c, counters(ctx), sizeof(c), cudaMemcpyDeviceToHost, ctx->last_stream));
+      TJ_CUDA(cudaStreamSynchronize(ctx->last_stream));
+    }
+    reserve_pairs(ctx, (unsigned long long)pairs, c.pairs, ctx->last_stream);
+  });
+}
+
+int tj_checkpoint_results(tj_ctx* ctx, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx) + 1, counters(ctx), sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int tj_rollback_results(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    if (cell_begin < 0 || cell_end > ctx->g.n_cells || cell_begin > cell_end)
+      fail(TJ_EINVAL, "cell range out of bounds");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->ctr_valid = false;
+    ctx->rows_range_done = false;
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx), counters(ctx) + 1, sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+    if (cell_end > cell_begin) {
+      zero_query_counts_kernel<<<kNumSMs * 4, 256, 0, s>>>(ctx->cell_start.as<int64_t>(),
+                                                           cell_begin, cell_end,
+                                                           ctx->qcount.as<uint32_t>());
+      TJ_CHECK_LAUNCH();
+    }
+  });
 }
 
 int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
@@ -271,10 +319,9 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
     const bool dmma = kernel == TJ_KERNEL_DMMA && norms_ok && g.d <= 64;
     const bool lowd = dmma && g.d_pad == 4;
-    if (!lowd && ctx->pair_cap == 0) {
-      const unsigned long long budget = free_budget(0.35, sizeof(uint2));
-      reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, budget), s);
-    }
+    if (!lowd && ctx->pair_cap == 0)  // callers size it (tj_reserve_results); a floor otherwise
+      reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, 1ull << 20),
+                    0, s);
     if (lowd) ensure_masks(ctx, s);
     // big cells at d_pad >= 12: the CTA-blocked Gram kernel (refine_gram.cu)
     const bool gram = dmma && !lowd && gram_applies(g.d_pad, g.n, g.n_cells);
@@ -356,13 +403,8 @@ int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed) {
     TJ_CUDA(cudaStreamSynchronize(s));
     ctx->ctr = c;
     ctx->ctr_valid = true;
-    *total = int64_t(c.pairs + c.hits);
-    const bool over_p = c.pairs > ctx->pair_cap;
-    if (overflowed) *overflowed = over_p ? 1 : 0;
-    if (over_p) {
-      reserve_pairs(ctx, c.pairs + c.pairs / 8, s);
-      zero_results(ctx, s);
-    }
+    *total = int64_t(c.pairs + c.hits);  // exact: appends are counted past the capacity
+    if (overflowed) *overflowed = c.pairs > ctx->pair_cap ? 1 : 0;
   });
 }
 

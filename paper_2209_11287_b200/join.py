@@ -335,8 +335,61 @@ class DeviceJoin:
                              estimated_pairs=[int(self.info.candidates)])
         return plan_from_estimates(self.ctx.cell_costs(self.info.n_cells), self.config.batch_size)
 
+    # ---- output-budget batcher (join.py:184-202) ----
+    SAMPLE_RANGES = 8          # contiguous cell ranges refined to estimate |R|
+    SAMPLE_SHARE = 1.0 / 256   # of the candidate pairs, per range
+    SAMPLE_ABOVE = 1 << 24     # candidate pairs below which the buffer is just sized to C
+
+    def appends_pairs(self) -> bool:
+        """Every kernel but the low-d DMMA one (hit masks) appends (query, candidate)
+        pairs to the ctx's pair buffer, whose size the batcher manages."""
+        return not (self.kernel == _native.TJ_KERNEL_DMMA and self.work.d_padded == 4)
+
+    def estimate_pairs(self, batches, costs=None) -> int:
+        """Result pairs of `batches`, estimated from a sampled refine: a few contiguous
+        cell ranges (each ~1/256 of the candidate pairs, spread over the batches) are
+        refined, their pair rate per candidate pair is extrapolated, +25% margin."""
+        if costs is None:
+            costs = self.ctx.cell_costs(self.info.n_cells)
+        csum = np.concatenate([[0], np.cumsum(costs)])
+        total_c = int(sum(csum[b] - csum[a] for a, b in batches))
+        if total_c <= self.SAMPLE_ABOVE:
+            return total_c
+        # sample ranges: starting points evenly spaced in candidate-pair order
+        cells, sampled = [], 0
+        offsets = np.linspace(0, total_c, self.SAMPLE_RANGES + 2)[1:-1]
+        acc, flat = 0, []
+        for a, b in batches:
+            flat.append((a, b, acc))
+            acc += int(csum[b] - csum[a])
+        for off in offsets:
+            for a, b, base in flat:
+                if base <= off < base + (csum[b] - csum[a]):
+                    c0 = int(np.searchsorted(csum, csum[a] + (off - base), side="right")) - 1
+                    want = csum[c0] + max(int(total_c * self.SAMPLE_SHARE), 1)
+                    c1 = min(b, max(c0 + 1, int(np.searchsorted(csum, want, side="left"))))
+                    cells.append((c0, c1))
+                    sampled += int(csum[c1] - csum[c0])
+                    break
+        self.ctx.reset_results()
+        self.ctx.reserve_results(sampled)
+        for c0, c1 in cells:
+            self.ctx.refine(self.kernel, self.config.short_circuit, c0, c1)
+        hits, _ = self.ctx.result_count()
+        self.ctx.reset_results()
+        rate = hits / max(sampled, 1)
+        return int(min(total_c, rate * total_c * 1.25 + 4096))
+
     def refine(self, cell_range=None, max_result_pairs=None, plan=None):
-        """Run every batch; returns the exact pair count (re-runs once on overflow)."""
+        """Run every batch; returns the exact pair count.
+
+        Appending kernels write into a pair buffer sized from a sampled estimate
+        (estimate_pairs).  The kernels count appends past its capacity, so after a
+        batch the exact total is known: an overflowing batch is rolled back
+        (counters + its per-query counts), the buffer grows to the exact size --
+        keeping the earlier batches' pairs -- and the batch runs again, so no
+        batch runs more than twice.  `max_result_pairs` is checked after every
+        batch (join.py:198-202)."""
         cfg = self.config
         if plan is None:
             plan = self.plan()
@@ -344,25 +397,42 @@ class DeviceJoin:
         if cell_range is not None:
             lo, hi = cell_range
             batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
-        for _attempt in range(2):
-            self.ctx.reset_results()
-            overflowed = False
-            for batch_no, (start, stop) in enumerate(batches):
-                self.ctx.refine(self.kernel, cfg.short_circuit, start, stop)
-                if max_result_pairs is not None:
-                    total, over = self.ctx.result_count()
-                    overflowed |= over
-                    if total > max_result_pairs:  # join.py:198-202
-                        raise ResourceError(
-                            f"batch {batch_no}: result grew to {total} pairs, "
-                            f"beyond the container capacity of {max_result_pairs}")
-                    if over:
-                        break
+        appends = self.appends_pairs()
+        if appends and batches:
+            est = self.estimate_pairs(batches)
+        self.ctx.reset_results()
+        if appends and batches:
+            self.ctx.reserve_results(est)
+        total = 0
+        for batch_no, (start, stop) in enumerate(batches):
+            if appends:
+                self.ctx.checkpoint_results()
+            self.ctx.refine(self.kernel, cfg.short_circuit, start, stop)
+            if not (appends or max_result_pairs is not None):
+                continue
             total, over = self.ctx.result_count()
-            if not (over or overflowed):
-                self.total = total
-                return total
-        raise RuntimeError("pair buffer overflowed twice")
+            if over:  # exact total known: roll back, grow, run the batch again
+                self.ctx.rollback_results(start, stop)
+                self.ctx.reserve_results(total + (total >> 4) + 1024)
+                self.ctx.refine(self.kernel, cfg.short_circuit, start, stop)
+                total, over = self.ctx.result_count()
+                if over:
+                    raise RuntimeError(f"batch {batch_no}: pair buffer overflowed after growing")
+            if max_result_pairs is not None and total > max_result_pairs:
+                raise ResourceError(
+                    f"batch {batch_no}: result grew to {total} pairs, "
+                    f"beyond the container capacity of {max_result_pairs}")
+        total, over = self.ctx.result_count()
+        if over:  # a kernel appended where none was expected (non-finite norms): redo once
+            self.ctx.reset_results()
+            self.ctx.reserve_results(total + 1024)
+            for start, stop in batches:
+                self.ctx.refine(self.kernel, cfg.short_circuit, start, stop)
+            total, over = self.ctx.result_count()
+            if over:
+                raise RuntimeError("pair buffer overflowed after growing")
+        self.total = total
+        return total
 
     def finalize(self):
         torch = self.torch

@@ -454,3 +454,48 @@ def test_gram_kernel_big_cells(n, d, k_idx, eps):
     tiles = int(np.sum(-(-nq // 8) * -(-cand // 8)))
     assert r.stats.tiles_processed == tiles
     assert r.stats.chunks_executed + r.stats.chunks_skipped == tiles * ((d + 3) // 4)
+
+
+# ------------------------------------------------------ output-budget batcher
+@pytest.mark.parametrize("kernel", ["scalar", "core_fma", "tile"])
+def test_pair_buffer_overflow_rolls_back_and_regrows(kernel, monkeypatch):
+    """A pair buffer far too small for the result (estimate forced to 1): every
+    overflowing batch is rolled back, the buffer grows to the exact count keeping the
+    earlier batches' pairs, and the batch re-runs -- the pair set is exact, the stats
+    count each batch once."""
+    from paper_2209_11287_b200.join import DeviceJoin
+
+    ds = generate(GenSpec("uniform", 6000, 5, seed=3))
+    eps = 0.12
+    want = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+    monkeypatch.setattr(DeviceJoin, "estimate_pairs", lambda self, batches, costs=None: 1)
+    for batch_size in (None, 2000, 50_000):
+        r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, batch_size=batch_size),
+                      max_result_pairs=10**9)
+        assert_oracle_equal(r, ds, eps)
+        assert r.stats.candidates_refined == want.stats.candidates_refined
+        assert r.stats.tiles_processed == want.stats.tiles_processed
+
+
+def test_small_join_then_large_batched_join_with_cap():
+    """a large batched join after a small one on the same context, with
+    max_result_pairs set, must not fail on the buffer the small join left behind."""
+    small = generate(GenSpec("uniform", 200, 6, seed=1))
+    self_join(small, JoinConfig(epsilon=0.2, kernel="scalar"))
+    ds = generate(GenSpec("uniform", 20_000, 6, seed=2))
+    eps = 0.15
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel="scalar", batch_size=100_000),
+                  max_result_pairs=10**9)
+    assert_oracle_equal(r, ds, eps)
+
+
+def test_pair_estimate_is_close_for_uniform_data():
+    from paper_2209_11287_b200.join import DeviceJoin
+
+    ds = generate(GenSpec("uniform", 200_000, 6, seed=4))
+    eps = 0.08
+    job = DeviceJoin(ds, JoinConfig(epsilon=eps, kernel="scalar"))
+    job.build()
+    est = job.estimate_pairs([(0, job.info.n_cells)])
+    total = job.refine()
+    assert total <= est <= 2 * total
