@@ -195,7 +195,8 @@ def refine_kernel_name(kernel: str, d: int) -> str:
 
 
 def traffic_from_profiles(config: str, kernel: str):
-    """DRAM bytes per refine launch from the committed ncu --set full summary, if any."""
+    """DRAM bytes per launch of `kernel` (function name) at `config`, from the committed
+    ncu --set full summary (profiles/ncu_summary.json), if any."""
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
         data = json.loads(p.read_text())
@@ -318,12 +319,23 @@ def run_reference(args, world, rank):
         "scaling": "weak" if world > 1 and args.scaling == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, seed 0)",
-        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps},
+        "config": workload_config(args, world),
         "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "TFLOP/s"},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host": host_info(),
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world: int) -> dict:
+    """The JSON line's `config`: identical in both arms (ours and --impl reference)."""
+    dist_name, n, d, eps = CONFIGS[args.config]
+    weak = world > 1 and args.scaling == "weak"
+    return {"workload": args.config, "dist": dist_name, "n": n * (world if weak else 1), "d": d,
+            "eps": eps, "kernel": args.kernel, "short_circuit": not args.no_short_circuit,
+            "l2": "256 MiB write between steps",
+            "parallelism": (f"weak: {world} slabs of the workload side by side along dim 0"
+                            if weak else f"strong: one workload over {world} rank(s)")}
 
 
 # ------------------------------------------------------------------ GPU side
@@ -424,6 +436,7 @@ def run_ours(args, world, rank, local):
                 "pairs": int(job.total),
                 "n_cells": int(info.n_cells),
                 "rechecks": int(st.guard_rechecks),
+                "emit_kernel_ms": job.ctx.last_emit_ms() if job.appends_pairs() is False else None,
             })
         return job
 
@@ -533,6 +546,33 @@ def run_ours(args, world, rank, local):
         costs = np.diff(cstart) * cand
         cpu = cpu_reference(ds, eps, d, C, costs, budget_s=args.cpu_budget)
     mean = lambda k: float(np.mean([t[k] for t in timings]))
+    # the dominant kernel by its measured share of the step: the refine (FP64
+    # roofline) or the row emission (HBM roofline, 4 B per result pair written)
+    refine_roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                   "frac": achieved / peak,
+                   "traffic": traffic_from_profiles(args.config, refine_kernel_name(args.kernel, d)),
+                   "kernel": refine_kernel_name(args.kernel, d),
+                   "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, DFMA "
+                                  f"{peak_dfma:.2f}) TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
+                   "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))",
+                   "share_of_step": share}
+    secondary = secondary_rooflines(n, d, dp, timings)
+    emit_ms = [t["emit_kernel_ms"] for t in timings if t.get("emit_kernel_ms")]
+    primary = refine_roof
+    if emit_ms:
+        e_ms = float(np.mean(emit_ms))
+        hbm, hbm_src = measured_hbm_gbs()
+        e_bytes = 4 * timings[0]["pairs"]
+        emit_roof = {"bound": "hbm", "achieved": e_bytes / (e_ms * 1e-3) / 1e9, "peak": hbm,
+                     "unit": "GB/s", "frac": e_bytes / (e_ms * 1e-3) / 1e9 / hbm,
+                     "traffic": traffic_from_profiles(args.config, "emit_rows_kernel"),
+                     "kernel": "emit_rows_kernel", "peak_source": hbm_src,
+                     "work": "4 B written per result pair (the canonical neighbour ids)",
+                     "ms": e_ms, "share_of_step": e_ms / float(np.mean([t["step_ms"] for t in timings]))}
+        if e_ms > ref_ms:
+            primary, secondary = emit_roof, [refine_roof] + secondary
+        else:
+            secondary = [emit_roof] + secondary
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -541,23 +581,15 @@ def run_ours(args, world, rank, local):
         "dtype": "f64",
         "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)"
                 if not weak else "synthetic: rank r = reference generator seed r, dim 0 shifted by r",
-        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps,
-                   "kernel": args.kernel, "short_circuit": cfg.short_circuit,
-                   "candidate_pairs": C, "result_pairs": timings[0]["pairs"],
-                   "n_cells": timings[0]["n_cells"], "l2": "256 MiB write between steps",
-                   "parallelism": (f"weak: {world} slabs of the workload side by side along dim 0, "
-                                   "rank r owns slab r's cells + a one-cell halo, no collectives "
-                                   "in the step") if weak else
-                                  f"cells split by estimated cost over {world} rank(s)"},
+        "config": workload_config(args, world),
+        "workload_stats": {"candidate_pairs": C, "result_pairs": timings[0]["pairs"],
+                           "n_cells": timings[0]["n_cells"],
+                           "layout": ("rank r owns slab r's cells + a one-cell halo, no "
+                                      "collectives in the step") if weak else "single device"},
         "phases_ms": {k: mean(k) for k in ("bcast_ms", "index_ms", "refine_ms", "refine_kernel_ms",
                                            "finalize_ms")},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profiles(args.config, args.kernel),
-                     "kernel": refine_kernel_name(args.kernel, d),
-                     "peak_source": f"in-run FP64 microbenchmark max(DMMA {peak_dmma:.2f}, DFMA {peak_dfma:.2f}) TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
-                     "work": "2*d FLOP per candidate pair (SURVEY.md 8(d))",
-                     "share_of_step": share},
-        "secondary_rooflines": secondary_rooflines(n, d, dp, timings),
+        "roofline": primary,
+        "secondary_rooflines": secondary,
         "tc_vs_core": {args.kernel: {"step_ms": step_ms, "refine_kernel_ms": ref_ms,
                                      "refine_tflops": achieved}} | {
             k: {"step_ms": o_step, "refine_kernel_ms": o_ref,
@@ -694,14 +726,11 @@ def run_strong(args, world, rank, local):
         "self_join_s": step_ms / 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator restated, seed 0; checksum pinned in tests/golden)",
-        "config": {"workload": args.config, "dist": dist_name, "n": n, "d": d, "eps": eps,
-                   "kernel": args.kernel, "short_circuit": cfg.short_circuit,
-                   "candidate_pairs": C, "result_pairs": total,
-                   "l2": "256 MiB write between steps",
-                   "parallelism": f"strong: one workload, {world} ranks own equal-cost "
-                                  "contiguous (x0, x1) bin ranges; NCCL all-reduce of bounds, "
-                                  "histogram and per-id counts + all-gather of the coordinates "
-                                  "inside the step"},
+        "config": workload_config(args, world),
+        "workload_stats": {"candidate_pairs": C, "result_pairs": total,
+                           "layout": f"{world} ranks own equal-cost contiguous (x0, x1) bin "
+                                     "ranges; NCCL all-reduce of bounds, histogram and per-id "
+                                     "counts + all-gather of the coordinates inside the step"},
         "phases_ms_max_over_ranks": phase_max,
         "rank0": {"n_local": timings[0]["n_local"], "pairs": timings[0]["rank_pairs"],
                   "refine_kernel_ms": ref_ms},

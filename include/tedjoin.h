@@ -259,6 +259,9 @@ int tj_dmma_known_answer(const double* a, const double* b, const double* c, doub
 /* Average duration (ms) of the last tj_refine launch's refine kernel, measured
  * with CUDA events on the launching stream (synchronous). */
 int tj_last_refine_ms(tj_ctx* ctx, double* ms);
+/* Duration (ms) of the last low-d row-emission kernel (emit_rows_kernel, the canonical
+ * output's dominant kernel), CUDA events on its stream (synchronous). */
+int tj_last_emit_ms(tj_ctx* ctx, double* ms);
 /* Kernels this library has launched so far in the process (all contexts). */
 int64_t tj_launch_count(void);
 

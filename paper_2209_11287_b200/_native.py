@@ -82,6 +82,7 @@ SIGNATURES = {
     "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
     "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_last_refine_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
+    "tj_last_emit_ms": (_i32, [_vp, ctypes.POINTER(_f64)]),
     "tj_launch_count": (_i64, []),
 }
 
@@ -340,6 +341,12 @@ class Context:
                                            int(n_rows), gid.data_ptr(),
                                            global_offsets.data_ptr(), int(dst_ptr),
                                            self.stream().cuda_stream))
+
+    def last_emit_ms(self) -> float | None:
+        ms = _f64()
+        if self.lib.tj_last_emit_ms(self.handle, ctypes.byref(ms)) != TJ_OK:
+            return None
+        return float(ms.value)
 
     def last_refine_ms(self) -> float:
         ms = _f64()

@@ -123,6 +123,8 @@ int tj_ctx_create(int device, tj_ctx** out) {
     c->device = device;
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
+    cudaEventCreate(&c->ev2);
+    cudaEventCreate(&c->ev3);
     *out = c;
   });
 }
@@ -141,6 +143,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
+  cudaEventDestroy(ctx->ev2);
+  cudaEventDestroy(ctx->ev3);
   cudaDeviceSynchronize();
   delete ctx;
 }
@@ -389,6 +393,17 @@ int tj_last_refine_ms(tj_ctx* ctx, double* ms) {
     TJ_CUDA(cudaEventSynchronize(ctx->ev1));
     float t = 0;
     TJ_CUDA(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+    *ms = t;
+  });
+}
+
+int tj_last_emit_ms(tj_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    if (!ctx->have_emit_timing) fail(TJ_EINVAL, "no row-emission launch recorded");
+    TJ_CUDA(cudaEventSynchronize(ctx->ev3));
+    float t = 0;
+    TJ_CUDA(cudaEventElapsedTime(&t, ctx->ev2, ctx->ev3));
     *ms = t;
   });
 }

@@ -921,6 +921,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
                                                             kEmitWarps * 32, smem));
       const int64_t grid = std::min<int64_t>(ceil_div(n_win, kEmitWarps),
                                              int64_t(kNumSMs) * std::max(per_sm, 1));
+      TJ_CUDA(cudaEventRecord(ctx->ev2, s));
       kern<<<unsigned(std::max<int64_t>(grid, 1)), kEmitWarps * 32, smem, s>>>(
           ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
           ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
@@ -928,6 +929,8 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
           ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
           offsets, n, nbr, long_rows, nbig + 2);
       TJ_CHECK_LAUNCH();
+      TJ_CUDA(cudaEventRecord(ctx->ev3, s));
+      ctx->have_emit_timing = true;
     }
     long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),

@@ -133,7 +133,9 @@ struct tj_ctx {
   int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
   int64_t n_items = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // around the last row-emission kernel
   bool have_refine_timing = false;
+  bool have_emit_timing = false;
   bool masks_ready = false;  // low-d mask layout built for the current grid
   bool ctr_valid = false;    // `ctr` holds the device counters (no refine since the read)
   tj::DevCounters ctr{};
