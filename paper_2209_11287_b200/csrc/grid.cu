@@ -15,6 +15,8 @@
 //     cell-ordered array, so a cell's candidate list is <= 3^(k-1) runs found by
 //     two binary searches each, already in the reference's concatenation order.
 #include <climits>
+#include <cmath>
+#include <cstring>
 
 #include "internal.cuh"
 #include "scan.cuh"
@@ -26,6 +28,19 @@ struct KeyParams {
   int shift[TJ_MAX_K_IDX];
   long long cmin[TJ_MAX_K_IDX];
 };
+
+// Signed integer image of a double with the same order (finite values and infinities).
+__host__ __device__ __forceinline__ long long ordered_bits(double v) {
+  long long b;
+  memcpy(&b, &v, sizeof(b));
+  return b >= 0 ? b : (b ^ 0x7fffffffffffffffll);
+}
+__host__ __device__ __forceinline__ double from_ordered_bits(long long b) {
+  if (b < 0) b ^= 0x7fffffffffffffffll;
+  double v;
+  memcpy(&v, &b, sizeof(v));
+  return v;
+}
 
 __device__ __forceinline__ long long cell_coord(double x, double eps) {
   return __double2ll_rd(__ddiv_rn(x, eps));  // floor(x / eps), IEEE division
@@ -40,35 +55,48 @@ __global__ void minmax_init_kernel(long long* mm, int k) {
   if (j == 0) mm[2 * TJ_MAX_K_IDX] = 0;  // max squared norm, as bits of a non-negative double
 }
 
+// Coordinate bounds per indexed dim.  floor(x / eps) is monotone in x for eps > 0
+// (IEEE division by a positive constant and floor both are), so the cell bounds
+// are floor(min x / eps) and floor(max x / eps): the kernel only compares raw
+// coordinates and the host divides the 2k extremes (bit-identical rounding).
 __global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int ld, int k,
                                    double eps, long long* mm) {
-  long long lo[TJ_MAX_K_IDX], hi[TJ_MAX_K_IDX];
+  (void)eps;
+  double lo[TJ_MAX_K_IDX], hi[TJ_MAX_K_IDX];
 #pragma unroll
   for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
-    lo[j] = LLONG_MAX;
-    hi[j] = LLONG_MIN;
+    lo[j] = INFINITY;
+    hi[j] = -INFINITY;
   }
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
+    const double* row = x + i * ld;
 #pragma unroll
-    for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+    for (int j = 0; j < TJ_MAX_K_IDX; j += 2) {
       if (j < k) {
-        long long c = cell_coord(x[i * ld + j], eps);
-        lo[j] = min(lo[j], c);
-        hi[j] = max(hi[j], c);
+        double2 v;
+        if (j + 1 < k && (ld & 1) == 0) v = *reinterpret_cast<const double2*>(row + j);
+        else v = make_double2(row[j], j + 1 < k ? row[j + 1] : row[j]);
+        lo[j] = fmin(lo[j], v.x);
+        hi[j] = fmax(hi[j], v.x);
+        if (j + 1 < k) {
+          lo[j + 1] = fmin(lo[j + 1], v.y);
+          hi[j + 1] = fmax(hi[j + 1], v.y);
+        }
       }
     }
   }
-  // warp -> block -> one atomic per block and dimension
-  __shared__ long long s_lo[TJ_MAX_K_IDX][32], s_hi[TJ_MAX_K_IDX][32];
+  // warp -> block -> one atomic per block and dimension (doubles as ordered bit
+  // patterns: min/max on the sign-adjusted integer image)
+  __shared__ double s_lo[TJ_MAX_K_IDX][32], s_hi[TJ_MAX_K_IDX][32];
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 #pragma unroll
   for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
     if (j >= k) break;
-    long long a = lo[j], b = hi[j];
+    double a = lo[j], b = hi[j];
     for (int o = 16; o > 0; o >>= 1) {
-      a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
-      b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
     }
     if (lane_id() == 0) {
       s_lo[j][warp] = a;
@@ -78,13 +106,13 @@ __global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int 
   __syncthreads();
   if (threadIdx.x < k) {
     const int j = threadIdx.x;
-    long long a = LLONG_MAX, b = LLONG_MIN;
+    double a = INFINITY, b = -INFINITY;
     for (int w = 0; w < nwarps; ++w) {
-      a = min(a, s_lo[j][w]);
-      b = max(b, s_hi[j][w]);
+      a = fmin(a, s_lo[j][w]);
+      b = fmax(b, s_hi[j][w]);
     }
-    atomicMin(&mm[2 * j], a);
-    atomicMax(&mm[2 * j + 1], b);
+    atomicMin(&mm[2 * j], ordered_bits(a));
+    atomicMax(&mm[2 * j + 1], ordered_bits(b));
   }
 }
 
@@ -371,12 +399,14 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   long long* mm = ctx->minmax.as<long long>();
   minmax_init_kernel<<<1, 32, 0, s>>>(mm, k);
   TJ_CHECK_LAUNCH();
-  cell_minmax_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 2 * kNumSMs)), 256, 0, s>>>(
+  cell_minmax_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 8 * kNumSMs)), 256, 0, s>>>(
       x, n, ld, k, eps, mm);
   TJ_CHECK_LAUNCH();
   long long hmm[2 * TJ_MAX_K_IDX];
   TJ_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(long long) * 2 * k, cudaMemcpyDeviceToHost, s));
   TJ_CUDA(cudaStreamSynchronize(s));
+  for (int j = 0; j < 2 * k; ++j)  // coordinate extremes -> cell extremes (grid.py:81)
+    hmm[j] = (long long)std::floor(from_ordered_bits(hmm[j]) / eps);
   int bits[TJ_MAX_K_IDX];
   int total_bits = 0;
   for (int j = 0; j < k; ++j) {
@@ -491,11 +521,13 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
   scan_exclusive(LoadAt<int64_t>{ctx->tmp64.as<int64_t>()},
                  StoreAt<int64_t>{ctx->cell_runs.as<int64_t>()}, nc, sc, s);
-  g.n_runs = read_scalar<int64_t>(sc.total, s);
-  TJ_CUDA(cudaMemcpyAsync(ctx->cell_runs.as<int64_t>() + nc, &g.n_runs, sizeof(int64_t),
-                          cudaMemcpyHostToDevice, s));
-  ctx->runs.ensure(sizeof(uint2) * std::max<int64_t>(g.n_runs, 1), s);
-  ctx->run_off.ensure(sizeof(uint32_t) * std::max<int64_t>(g.n_runs, 1), s);
+  // the run count stays on the device (read back with the totals below): the run
+  // table is sized for its bound, 3^(k-1) rows per cell
+  TJ_CUDA(cudaMemcpyAsync(ctx->cell_runs.as<int64_t>() + nc, sc.total, sizeof(int64_t),
+                          cudaMemcpyDeviceToDevice, s));
+  const int64_t runs_bound = std::max<int64_t>(nc * rp.n_rows, 1);
+  ctx->runs.ensure(sizeof(uint2) * runs_bound, s);
+  ctx->run_off.ensure(sizeof(uint32_t) * runs_bound, s);
   cand_fill_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
                                                ctx->cell_start.as<int64_t>(), nc,
                                                ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
@@ -511,6 +543,8 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   TJ_CHECK_LAUNCH();
   unsigned long long ht[3];
   unsigned long long maxnorm_bits;
+  TJ_CUDA(cudaMemcpyAsync(&g.n_runs, ctx->cell_runs.as<int64_t>() + nc, sizeof(int64_t),
+                          cudaMemcpyDeviceToHost, s));
   TJ_CUDA(cudaMemcpyAsync(ht, totals, sizeof(ht), cudaMemcpyDeviceToHost, s));
   TJ_CUDA(cudaMemcpyAsync(&maxnorm_bits, mm + 2 * TJ_MAX_K_IDX, sizeof(maxnorm_bits),
                           cudaMemcpyDeviceToHost, s));
