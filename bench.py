@@ -46,6 +46,8 @@ CONFIGS = {  # BASELINE.md §2 / SURVEY.md §8(d); eps for ~64 neighbours per po
     "c4d32": ("uniform", 2_000_000, 32, 1.31923),
     "c4d64": ("uniform", 2_000_000, 64, 2.27218),
     "c5": ("uniform", 50_000_000, 4, 0.0232204),
+    # the paper's best case (Expo3D2M): skewed 3-D data at ~64 neighbours
+    "expo3d2m": ("exponential", 2_000_000, 3, 0.00097345),
 }
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 

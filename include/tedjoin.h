@@ -137,14 +137,15 @@ int tj_finalize(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, void* stream
 int tj_finalize_offsets(tj_ctx* ctx, int64_t* offsets, void* stream);
 int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, void* stream);
 
-/* The rows of the original ids [id_begin, id_end) only, into their CSR places
- * (offsets from tj_finalize_offsets).  Once the stream reaches the end of this
- * call the range's part of neighbors is final, so a caller can copy it to the
- * host while the next range is built (the pinned, chunked result pipeline of
- * DeviceJoin.finalize_fetch).  Low-d DMMA results are emitted straight by id;
- * for other kernels the first call builds every row.  Asynchronous. */
-int tj_finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
-                           int64_t id_begin, int64_t id_end, void* stream);
+/* The rows of one of `chunks` (<= 256) equal original-id ranges only: chunk j
+ * covers ids [ceil(j n / chunks), ceil((j+1) n / chunks)), one contiguous part of
+ * the CSR (offsets from tj_finalize_offsets).  Once the stream passes this call
+ * the part is final, so a caller copies it to the host while the next chunk is
+ * built (the chunked, pinned result pipeline of DeviceJoin.finalize_fetch).  Low-d
+ * DMMA results are emitted per chunk from the hit masks; for other kernels the
+ * first call builds every row.  Asynchronous. */
+int tj_finalize_rows_chunk(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
+                           int32_t chunk, int32_t chunks, void* stream);
 
 /* Counters accumulated since the last tj_reset_results (synchronous). */
 int tj_get_stats(tj_ctx* ctx, tj_stats* out);

@@ -58,7 +58,7 @@ SIGNATURES = {
     "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_finalize_offsets": (_i32, [_vp, _vp, _vp]),
     "tj_finalize_rows": (_i32, [_vp, _vp, _vp, _vp]),
-    "tj_finalize_rows_range": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "tj_finalize_rows_chunk": (_i32, [_vp, _vp, _vp, _i32, _i32, _vp]),
     "tj_get_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
     "tj_cell_costs": (_i32, [_vp, _vp]),
     "tj_pair_sq_dists": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp]),
@@ -228,11 +228,11 @@ class Context:
             self.handle, offsets.data_ptr(),
             neighbors.data_ptr() if neighbors is not None else None, s.cuda_stream))
 
-    def finalize_rows_range(self, offsets, neighbors, id_begin: int, id_end: int, stream=None):
+    def finalize_rows_chunk(self, offsets, neighbors, chunk: int, chunks: int, stream=None):
         s = stream or self.stream()
-        self._check(self.lib.tj_finalize_rows_range(
+        self._check(self.lib.tj_finalize_rows_chunk(
             self.handle, offsets.data_ptr(), neighbors.data_ptr() if neighbors is not None else None,
-            int(id_begin), int(id_end), s.cuda_stream))
+            int(chunk), int(chunks), s.cuda_stream))
 
     def stats(self) -> Stats:
         st = Stats()

@@ -471,12 +471,13 @@ int tj_finalize_rows(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors, v
   });
 }
 
-int tj_finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
-                           int64_t id_begin, int64_t id_end, void* stream) {
+int tj_finalize_rows_chunk(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighbors,
+                           int32_t chunk, int32_t chunks, void* stream) {
   if (!ctx || !offsets) return TJ_EINVAL;
   return guarded(ctx, [&] {
     require_grid(ctx);
-    if (id_begin < 0 || id_end > ctx->g.n || id_begin > id_end) fail(TJ_EINVAL, "id range out of bounds");
+    if (chunks < 1 || chunks > 256 || chunk < 0 || chunk >= chunks)
+      fail(TJ_EINVAL, "need 0 <= chunk < chunks <= 256");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
     DevCounters c = ctx->ctr;
@@ -491,7 +492,7 @@ int tj_finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* neighb
     if (c.pairs + c.hits > 0 && !neighbors) fail(TJ_EINVAL, "neighbors is null");
     if (c.pairs + c.hits == 0) return;
     finalize_rows_range(ctx, offsets, neighbors, int64_t(c.pairs), int64_t(c.hits),
-                        int64_t(c.max_row), id_begin, id_end, s);
+                        int64_t(c.max_row), chunk, chunks, s);
   });
 }
 

@@ -390,7 +390,17 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
-template <int MINB>
+// LIST = false: windows of 32 consecutive positions.  LIST = true: windows of 32
+// consecutive entries of a position list (ascending positions of the rows of one
+// original-id range, tj_finalize_rows_chunk): the rows land at the same final
+// places, but the range is complete when the launch ends.
+struct RowList {
+  const uint32_t* pos;   // ascending positions
+  int64_t begin, end;    // entries of this launch
+  const uint32_t* pcell; // cell of every position
+};
+
+template <int MINB, bool LIST>
 __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     emit_rows_kernel(const unsigned long long* __restrict__ masks,
                      const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
@@ -399,23 +409,38 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
                      int64_t n_cells, const uint32_t* __restrict__ win_cell,
                      const uint32_t* __restrict__ qcount, const uint32_t* __restrict__ perm,
                      const int64_t* __restrict__ offsets, int64_t n, uint32_t* __restrict__ nbr,
-                     uint32_t* __restrict__ long_rows, unsigned long long* n_long) {
+                     uint32_t* __restrict__ long_rows, unsigned long long* n_long, RowList rl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   EmitSmem& sm = reinterpret_cast<EmitSmem*>(smem_raw)[warp];
   uint32_t* pool = sm.pool;
-  const int64_t n_win = (n + 31) >> 5;
+  const int64_t n_win = LIST ? (rl.end - rl.begin + 31) >> 5 : (n + 31) >> 5;
   const int64_t stride = int64_t(gridDim.x) * kEmitWarps;
   for (int64_t w = int64_t(blockIdx.x) * kEmitWarps + warp; w < n_win; w += stride) {
-    const int64_t p0 = w << 5, p = p0 + lane;
-    const bool valid = p < n;
+    int64_t p;
+    bool valid;
+    if constexpr (LIST) {
+      const int64_t e = rl.begin + (w << 5) + lane;
+      valid = e < rl.end;
+      p = valid ? int64_t(rl.pos[e]) : 0;
+    } else {
+      p = (w << 5) + lane;
+      valid = p < n;
+    }
     const int len = valid ? int(qcount[p]) : 0;
     // windows of cells another rank / batch refined: nothing to do
     if (__ballot_sync(0xffffffffu, len > 0) == 0u) continue;
     const uint32_t id = valid ? perm[p] : 0u;
     const int64_t dst = valid ? offsets[id] : 0;
-    const int64_t c0 = win_cell[w];
-    const int64_t c = window_lane_cell(cell_start, n_cells, c0, p0);
+    int64_t c0, c;
+    if constexpr (LIST) {  // positions ascend along the window: lane 0 has the first cell
+      c = valid ? int64_t(rl.pcell[p]) : -1;
+      c0 = __shfl_sync(0xffffffffu, c, 0);
+      if (!valid) c = c0;
+    } else {
+      c0 = win_cell[w];
+      c = window_lane_cell(cell_start, n_cells, c0, w << 5);
+    }
     const bool pooled = len > 0 && len <= kPoolSlots;
     if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = uint32_t(p);
     MaskRow mr{};
@@ -511,97 +536,16 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
   }
 }
 
-// Id-ordered variant of emit_rows_kernel for the host-output pipeline: a warp
-// takes 32 consecutive ORIGINAL ids [id_begin + 32 w, +32) of one id range, so
-// the rows it writes form one contiguous segment of the CSR and a range is final
-// as soon as its launch ends -- its D2H can then overlap the next range's emit
-// (tj_finalize_rows_range).  Per lane: position ipos[id], cell pcell[position],
-// the same mask walk / pool / sort as emit_rows_kernel; offsets map to positions
-// by a binary search of the lane's own run table (lanes of a window sit in
-// unrelated cells, so nothing is staged per window).  Longer rows are listed for
-// long_rows_kernel by position.
-__global__ void __launch_bounds__(kEmitWarps * 32, 4)
-    emit_ids_kernel(const unsigned long long* __restrict__ masks,
-                    const int64_t* __restrict__ cell_mbase, const int64_t* __restrict__ cell_start,
-                    const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
-                    const uint32_t* __restrict__ run_off, const int64_t* __restrict__ cell_cand,
-                    const uint32_t* __restrict__ ipos, const uint32_t* __restrict__ pcell,
-                    const uint32_t* __restrict__ perm, const int64_t* __restrict__ offsets,
-                    int64_t id_begin, int64_t id_end, uint32_t* __restrict__ nbr,
-                    uint32_t* __restrict__ long_rows, unsigned long long* n_long) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  uint32_t* pool = reinterpret_cast<uint32_t*>(smem_raw) + warp * kPoolSlots * kPoolLd;
-  const int64_t n_win = (id_end - id_begin + 31) >> 5;
-  const int64_t stride = int64_t(gridDim.x) * kEmitWarps;
-  for (int64_t w = int64_t(blockIdx.x) * kEmitWarps + warp; w < n_win; w += stride) {
-    const int64_t id = id_begin + (w << 5) + lane;
-    const bool valid = id < id_end;
-    const int64_t dst = valid ? offsets[id] : 0;
-    const int len = valid ? int(offsets[id + 1] - dst) : 0;
-    if (__ballot_sync(0xffffffffu, len > 0) == 0u) continue;
-    const uint32_t p = valid ? ipos[id] : 0u;
-    const bool pooled = len > 0 && len <= kPoolSlots;
-    if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = p;
-    uint32_t* col = pool + lane;
-    if (pooled) {
-      const int64_t c = pcell[p];
-      const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, int64_t(p) - cell_start[c]);
-      for (int b = 0; b < mr.nblk; b += 4) prefetch_l1(mr.m + b);
-      int slot = 0;
-      for (int b0 = 0; b0 < mr.nblk; b0 += 16) {
-        unsigned long long mv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) mv[u] = b0 + u < mr.nblk ? mr.m[b0 + u] : 0ull;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          unsigned wbits = 0u;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) wbits |= row_bits(mv[4 * q + u], mr.shift) << u;
-          while (wbits) {
-            const int j = __ffs(wbits) - 1;
-            wbits &= wbits - 1u;
-            col[slot * kPoolLd] = uint32_t(8 * (b0 + 4 * q + (j & 3)) + (j >> 2));
-            ++slot;
-          }
-        }
-      }
-      const int64_t rb = cell_runs[c];
-      const int nr = int(cell_runs[c + 1] - rb);
-      for (int i0 = 0; i0 < len; i0 += 16) {  // offsets -> positions -> ids, 16 in flight
-        uint32_t v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          v[u] = i0 + u < len ? run_position(runs, run_off, rb, nr, col[(i0 + u) * kPoolLd]) : 0u;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = i0 + u < len ? __ldg(perm + v[u]) : 0u;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (i0 + u < len) col[(i0 + u) * kPoolLd] = v[u];
-      }
-    }
-    __syncwarp();
-    pool_sort(pool, pooled ? len : 0);
-    __syncwarp();
-    const unsigned todo = __ballot_sync(0xffffffffu, pooled);
-    for (unsigned m = todo; m; m &= m - 1u) {
-      const int k = __ffs(m) - 1;
-      const int L = __shfl_sync(0xffffffffu, len, k);
-      const int64_t D = __shfl_sync(0xffffffffu, dst, k);
-#pragma unroll
-      for (int e0 = 0; e0 < kPoolSlots; e0 += 32)
-        if (e0 + lane < L) nbr[D + e0 + lane] = pool[(e0 + lane) * kPoolLd + k];
-    }
-  }
-}
-
-// ipos[perm[p]] = p (position of every original id); pcell[p] = cell of position p.
-__global__ void id_maps_kernel(const uint32_t* __restrict__ perm, const int64_t* __restrict__ cell_start,
-                               int64_t n, int64_t n_cells, uint32_t* __restrict__ ipos,
-                               uint32_t* __restrict__ pcell) {
+// pcell[p] = cell of position p; key[p] = the original-id range (of `chunks`
+// equal ranges) holding perm[p] -- a stable sort by key lists every range's
+// positions in ascending order (tj_finalize_rows_chunk).
+__global__ void chunk_keys_kernel(const uint32_t* __restrict__ perm,
+                                  const int64_t* __restrict__ cell_start, int64_t n,
+                                  int64_t n_cells, int chunks, uint64_t* __restrict__ key,
+                                  uint32_t* __restrict__ pcell) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
        p += int64_t(gridDim.x) * blockDim.x)
-    ipos[perm[p]] = uint32_t(p);
+    key[p] = uint64_t((int64_t(perm[p]) * chunks) / n);
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
        c += int64_t(gridDim.x) * blockDim.x)
     for (int64_t p = cell_start[c]; p < cell_start[c + 1]; ++p) pcell[p] = uint32_t(c);
@@ -824,12 +768,15 @@ static void sort_big_rows(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, uint32_t
   hb.release(s);
 }
 
-// Rows of the original ids [id_begin, id_end) (offsets from phase 1).  Low-d
-// mask results are emitted by id (emit_ids_kernel); other results have no
-// per-id source, so the first call builds every row (later calls find them done).
+// Rows of id range `chunk` of the split of [0, n) into `chunks` equal ranges
+// (offsets from phase 1).  Low-d mask
+// results: the range's positions (a stable partition of the positions by id
+// range, built once per grid) are emitted by emit_rows_kernel<LIST>, windows of
+// 32 ascending positions.  Other results have no per-id source, so the first call
+// builds every row (later calls find them done).
 void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
-                         int64_t n_mask_hits, int64_t max_mask_row, int64_t id_begin,
-                         int64_t id_end, cudaStream_t s) {
+                         int64_t n_mask_hits, int64_t max_mask_row, int chunk, int chunks,
+                         cudaStream_t s) {
   const int64_t n = ctx->g.n;
   if (n_mask_hits == 0) {
     if (!ctx->rows_range_done)
@@ -837,38 +784,57 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
     ctx->rows_range_done = true;
     return;
   }
-  if (id_end <= id_begin) return;
-  if (!ctx->id_maps_ready) {
-    ctx->ipos.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1), s);
+  // the chunk lists: positions of every id range, ascending (once per grid and K)
+  const int K = int(std::min<int64_t>(std::max<int64_t>(chunks, 1), 256));
+  if (!ctx->id_maps_ready || ctx->chunk_lists != K) {
     ctx->pcell.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1), s);
-    id_maps_kernel<<<blocks_for(std::max(n, ctx->g.n_cells), 256), 256, 0, s>>>(
-        ctx->perm.as<uint32_t>(), ctx->cell_start.as<int64_t>(), n, ctx->g.n_cells,
-        ctx->ipos.as<uint32_t>(), ctx->pcell.as<uint32_t>());
+    ctx->chunk_key.ensure(sizeof(uint64_t) * 2 * std::max<int64_t>(n, 1), s);
+    ctx->ipos.ensure(sizeof(uint32_t) * 2 * std::max<int64_t>(n, 1), s);
+    uint64_t* k0 = ctx->chunk_key.as<uint64_t>();
+    uint32_t* v0 = ctx->ipos.as<uint32_t>();
+    chunk_keys_kernel<<<blocks_for(std::max(n, ctx->g.n_cells), 256), 256, 0, s>>>(
+        ctx->perm.as<uint32_t>(), ctx->cell_start.as<int64_t>(), n, ctx->g.n_cells, K, k0,
+        ctx->pcell.as<uint32_t>());
     TJ_CHECK_LAUNCH();
+    DevBuf hb;
+    hb.ensure(sizeof(int64_t) * radix_sort_scratch_elems(n), s);
+    ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(radix_sort_scratch_elems(n), n), s);
+    int kb = 0;
+    while ((1 << kb) < K) ++kb;
+    const int where = radix_sort_pairs(k0, v0, k0 + n, v0 + n, n, std::max(kb, 1), true,
+                                       hb.as<int64_t>(), sc, s);
+    ctx->chunk_pos_off = where ? n : 0;
+    hb.release(s);
+    ctx->chunk_lists = K;
     ctx->id_maps_ready = true;
   }
+  // chunk j holds the ids [ceil(j n / K), ceil((j+1) n / K)): one position each,
+  // so its list entries start after the ceil(j n / K) positions of smaller ids
+  auto first_entry = [&](int64_t j) -> int64_t { return (j * n + K - 1) / K; };
+  const int64_t lb = first_entry(chunk), le = first_entry(chunk + 1);
   ctx->fill.ensure(sizeof(uint32_t) * n + 4 * sizeof(unsigned long long), s);
   uint32_t* fill = ctx->fill.as<uint32_t>();
   unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
   TJ_CUDA(cudaMemsetAsync(nbig, 0, 3 * sizeof(unsigned long long), s));
   ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
   uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
-  const size_t smem = sizeof(uint32_t) * kPoolSlots * kPoolLd * kEmitWarps;
-  TJ_CUDA(cudaFuncSetAttribute(emit_ids_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  int per_sm = 0;
-  TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_ids_kernel,
-                                                        kEmitWarps * 32, smem));
-  const int64_t n_win = ceil_div(id_end - id_begin, 32);
-  const int64_t grid = std::min<int64_t>(ceil_div(n_win, kEmitWarps),
-                                         int64_t(kNumSMs) * std::max(per_sm, 1));
-  emit_ids_kernel<<<unsigned(std::max<int64_t>(grid, 1)), kEmitWarps * 32, smem, s>>>(
-      ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
-      ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
-      ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->ipos.as<uint32_t>(),
-      ctx->pcell.as<uint32_t>(), ctx->perm.as<uint32_t>(), offsets, id_begin, id_end, nbr,
-      long_rows, nbig + 2);
-  TJ_CHECK_LAUNCH();
+  if (le > lb) {
+    auto kern = emit_rows_kernel<4, true>;
+    const size_t smem = sizeof(EmitSmem) * kEmitWarps;
+    TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmitWarps * 32, smem));
+    const int64_t grid = std::min<int64_t>(ceil_div(ceil_div(le - lb, 32), kEmitWarps),
+                                           int64_t(kNumSMs) * std::max(per_sm, 1));
+    RowList rl{ctx->ipos.as<uint32_t>() + ctx->chunk_pos_off, lb, le, ctx->pcell.as<uint32_t>()};
+    kern<<<unsigned(std::max<int64_t>(grid, 1)), kEmitWarps * 32, smem, s>>>(
+        ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
+        ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+        ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
+        ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
+        offsets, n, nbr, long_rows, nbig + 2, rl);
+    TJ_CHECK_LAUNCH();
+  }
   long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
@@ -912,7 +878,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     {
       // 4 CTAs/SM (<= 128 registers): measured on par with the unbounded build
       // (158 registers, 3 CTAs) and well ahead of 5 CTAs (spills)
-      auto kern = emit_rows_kernel<4>;
+      auto kern = emit_rows_kernel<4, false>;
       const size_t smem = sizeof(EmitSmem) * kEmitWarps;
       TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
@@ -927,7 +893,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
           ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
           ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc,
           ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
-          offsets, n, nbr, long_rows, nbig + 2);
+          offsets, n, nbr, long_rows, nbig + 2, RowList{});
       TJ_CHECK_LAUNCH();
       TJ_CUDA(cudaEventRecord(ctx->ev3, s));
       ctx->have_emit_timing = true;

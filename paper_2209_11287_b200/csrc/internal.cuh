@@ -126,8 +126,11 @@ struct tj_ctx {
   // results
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
-  tj::DevBuf ipos, pcell;        // id -> position, position -> cell (id-ordered emit)
-  bool id_maps_ready = false;    // ipos / pcell built for the current grid
+  tj::DevBuf ipos, pcell;        // id-range position lists (2 x n: sort ping-pong), position -> cell
+  tj::DevBuf chunk_key;          // sort keys of the position lists
+  int64_t chunk_pos_off = 0;     // which half of ipos holds the sorted lists
+  int chunk_lists = 0;           // id ranges the lists were built for
+  bool id_maps_ready = false;    // lists / pcell built for the current grid
   bool rows_range_done = false;  // pair-path rows built by an earlier range call
   unsigned long long pair_cap = 0;
   int64_t mask_cells_begin = 0, mask_cells_end = 0;  // cells whose masks are in `masks`
@@ -207,6 +210,6 @@ void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* 
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,
                   int64_t n_mask_hits, int64_t max_mask_row, cudaStream_t s, int phase = 3);
 void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
-                         int64_t n_mask_hits, int64_t max_mask_row, int64_t id_begin,
-                         int64_t id_end, cudaStream_t s);
+                         int64_t n_mask_hits, int64_t max_mask_row, int chunk, int chunks,
+                         cudaStream_t s);
 }  // namespace tj

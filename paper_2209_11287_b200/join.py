@@ -458,7 +458,7 @@ class DeviceJoin:
 
         The offsets go first (their D2H on the copy stream overlaps the first rows).
         The rows are then built in `chunks` ranges of original ids
-        (tj_finalize_rows_range): each range is one contiguous part of the CSR, final
+        (tj_finalize_rows_chunk): each range is one contiguous part of the CSR, final
         when its kernels end, and its D2H on the copy stream overlaps the next range's
         emit -- the double-buffered result pipeline of the north star, with the PCIe
         copy engine running while the SMs emit."""
@@ -479,10 +479,10 @@ class DeviceJoin:
             off.copy_(self.offsets_d, non_blocking=True)
             off_ready = torch.cuda.Event()
             off_ready.record(cs)
-        bounds = [n * k // chunks for k in range(chunks + 1)]
+        bounds = [(k * n + chunks - 1) // chunks for k in range(chunks + 1)]  # tj_finalize_rows_chunk
         for k in range(chunks):
             a, b = bounds[k], bounds[k + 1]
-            self.ctx.finalize_rows_range(self.offsets_d, self.neighbors_d, a, b)
+            self.ctx.finalize_rows_chunk(self.offsets_d, self.neighbors_d, k, chunks)
             done = torch.cuda.Event()
             done.record(main)
             if k == 0:

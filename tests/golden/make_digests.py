@@ -39,6 +39,7 @@ CONFIGS = {
     "c5": ("uniform", 50_000_000, 4, 0.0232204),
     "c4d8": ("uniform", 2_000_000, 8, 0.244686),
     "c3": ("exponential", 5_000_000, 8, 0.0118508),
+    "expo3d2m": ("exponential", 2_000_000, 3, 0.00097345),
     # brute force over 4e12 candidate pairs: hours on 8 cores, run in the background
     "c4d16": ("uniform", 2_000_000, 16, 0.657508),
     "c4d32": ("uniform", 2_000_000, 32, 1.31923),
@@ -57,8 +58,9 @@ def main(names):
         dg.update({"dist": dist, "n": n, "d": d, "eps": eps, "checksum": ds.checksum(),
                    "oracle_seconds": round(time.perf_counter() - t, 1),
                    "oracle_threads": oracle.num_threads()})
-        out[name] = dg
         print(name, dg, flush=True)
+        out = json.loads(path.read_text()) if path.exists() else {}  # entries written meanwhile
+        out[name] = dg
         path.write_text(json.dumps(out, indent=1))
 
 
