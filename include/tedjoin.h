@@ -116,6 +116,15 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
  * (the output-budget batcher of DeviceJoin.refine, join.py:184-202). */
 int tj_result_count(tj_ctx* ctx, int64_t* total, int32_t* overflowed);
 int tj_reset_results(tj_ctx* ctx, void* stream);
+/* Sampled selectivity estimate for sizing the pair buffer (the output-budget
+ * batcher): `samples` work items -- cells of [cell_begin, cell_end) drawn with
+ * probability |cell|*|cand| (join.py:122-124), one query block at a random offset
+ * against the cell's whole candidate list -- run on `kernel`'s refine kernel with
+ * nothing stored; *pairs_per_candidate = result pairs / candidate pairs of the
+ * sample.  Counters and per-query counts are left as they were.  Not for the low-d
+ * DMMA kernel (hit masks, nothing to size).  Synchronous. */
+int tj_estimate_pairs(tj_ctx* ctx, int32_t kernel, int64_t cell_begin, int64_t cell_end,
+                      int32_t samples, uint64_t seed, double* pairs_per_candidate, void* stream);
 /* Grow the pair append buffer to `pairs` entries, keeping what was appended so far. */
 int tj_reserve_results(tj_ctx* ctx, int64_t pairs);
 /* Snapshot the result counters (stream-ordered) before a batch ... */

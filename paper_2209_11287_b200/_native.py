@@ -54,6 +54,8 @@ SIGNATURES = {
     "tj_reset_results": (_i32, [_vp, _vp]),
     "tj_reserve_results": (_i32, [_vp, _i64]),
     "tj_checkpoint_results": (_i32, [_vp, _vp]),
+    "tj_estimate_pairs": (_i32, [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64,
+                                 ctypes.POINTER(_f64), _vp]),
     "tj_rollback_results": (_i32, [_vp, _i64, _i64, _vp]),
     "tj_finalize": (_i32, [_vp, _vp, _vp, _vp]),
     "tj_finalize_offsets": (_i32, [_vp, _vp, _vp]),
@@ -197,6 +199,16 @@ class Context:
 
     def reserve_results(self, pairs: int):
         self._check(self.lib.tj_reserve_results(self.handle, int(pairs)))
+
+    def estimate_pairs(self, kernel: int, cell_begin: int, cell_end: int, samples: int = 256,
+                       seed: int = 0, stream=None) -> float:
+        """Sampled result pairs per candidate pair of the cell range (tj_estimate_pairs)."""
+        s = stream or self.stream()
+        rate = _f64()
+        self._check(self.lib.tj_estimate_pairs(self.handle, int(kernel), int(cell_begin),
+                                               int(cell_end), int(samples), int(seed),
+                                               ctypes.byref(rate), s.cuda_stream))
+        return float(rate.value)
 
     def checkpoint_results(self, stream=None):
         s = stream or self.stream()

@@ -303,6 +303,78 @@ int tj_rollback_results(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, void*
   });
 }
 
+// Which refine kernel a tj_refine call runs and how it cuts work items.
+struct RefinePlan {
+  bool lowd, dmma, gram;
+  int variant;     // CUDA-core variant (refine_core.cu)
+  int qpi;         // queries per work item
+  int64_t target;  // candidate-slice target of build_work_items
+};
+
+static RefinePlan plan_refine(const tj_ctx* ctx, int32_t kernel) {
+  const GridState& g = ctx->g;
+  RefinePlan r{};
+  // The expanded form needs finite norms; beyond that the exact kernel decides.
+  const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
+  r.dmma = kernel == TJ_KERNEL_DMMA && norms_ok && g.d <= 64;
+  r.lowd = r.dmma && g.d_pad == 4;
+  // big cells at d_pad >= 12: the CTA-blocked Gram kernel (refine_gram.cu)
+  r.gram = r.dmma && !r.lowd && gram_applies(g.d_pad, g.n, g.n_cells);
+  r.variant = kernel == TJ_KERNEL_CORE_FMA                   ? 1
+              : kernel == TJ_KERNEL_CORE_EXPANDED && norms_ok ? 2
+                                                              : 0;
+  r.qpi = r.lowd   ? lowd_queries_per_item(g.n, g.n_cells)
+          : r.gram ? kGramQueries
+          : r.dmma ? tc_queries_per_item(g.d_pad, g.n, g.n_cells)
+                   : core_queries_per_item(g.d, g.d_pad);
+  // lowd: items never split a candidate list (each query row comes from one item);
+  // gram: 64-query items x 32k-candidate slices
+  r.target = r.lowd   ? (int64_t(1) << 60)
+             : r.gram ? int64_t(kGramQueries) * kGramSlice
+                      : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
+  return r;
+}
+
+static RefineArgs refine_args(tj_ctx* ctx, const RefinePlan& rp, int32_t short_circuit) {
+  const GridState& g = ctx->g;
+  RefineArgs a{};
+  a.P = ctx->P.as<double>();
+  a.NRM = ctx->NRM.as<double>();
+  a.CN = ctx->CN.as<double>();
+  a.SFX = ctx->SFX.as<double>();
+  a.runs = ctx->runs.as<uint2>();
+  a.run_off = ctx->run_off.as<uint32_t>();
+  a.cell_runs = ctx->cell_runs.as<int64_t>();
+  a.cell_start = ctx->cell_start.as<int64_t>();
+  a.items = ctx->items.as<WorkItem>();
+  a.n_items = ctx->n_items;
+  a.n_items_dev = rp.lowd ? &counters(ctx)->n_items : nullptr;
+  a.ctr = counters(ctx);
+  a.pairs = ctx->pairs.as<uint2>();
+  a.pair_cap = ctx->pair_cap;
+  a.qcount = ctx->qcount.as<uint32_t>();
+  a.masks = ctx->masks.as<unsigned long long>();
+  a.cell_mbase = ctx->cell_mbase.as<int64_t>();
+  a.cell_base = 0;
+  a.d = g.d;
+  a.d_pad = g.d_pad;
+  a.nchunks = g.nchunks;
+  a.eps_sq = g.eps_sq;
+  a.guard_rel = guard_rel(g.d, g.d_pad);
+  a.max_norm = g.max_norm + g.eps_sq;
+  a.short_circuit = short_circuit ? 1 : 0;
+  return a;
+}
+
+static void launch_refine(const tj_ctx* ctx, const RefinePlan& rp, const RefineArgs& a,
+                          cudaStream_t s) {
+  const GridState& g = ctx->g;
+  if (rp.lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
+  else if (rp.gram) launch_refine_gram(a, s);
+  else if (rp.dmma) launch_refine_tc(a, g.n, g.n_cells, s);
+  else launch_refine_core(a, rp.variant, s);
+}
+
 int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
               int64_t cell_end, void* stream) {
   if (!ctx) return TJ_EINVAL;
@@ -319,70 +391,111 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     ctx->ctr_valid = false;
     ctx->rows_range_done = false;
     if (cell_begin == cell_end) return;
-    // The expanded form needs finite norms; beyond that the exact kernel decides.
-    const bool norms_ok = std::isfinite(g.max_norm) && g.max_norm < 1e290;
-    const bool dmma = kernel == TJ_KERNEL_DMMA && norms_ok && g.d <= 64;
-    const bool lowd = dmma && g.d_pad == 4;
-    if (!lowd && ctx->pair_cap == 0)  // callers size it (tj_reserve_results); a floor otherwise
+    const RefinePlan rp = plan_refine(ctx, kernel);
+    if (!rp.lowd && ctx->pair_cap == 0)  // callers size it (tj_reserve_results); a floor otherwise
       reserve_pairs(ctx, std::min<unsigned long long>((unsigned long long)g.candidates, 1ull << 20),
                     0, s);
-    if (lowd) ensure_masks(ctx, s);
-    // big cells at d_pad >= 12: the CTA-blocked Gram kernel (refine_gram.cu)
-    const bool gram = dmma && !lowd && gram_applies(g.d_pad, g.n, g.n_cells);
-    const int qpi = lowd   ? lowd_queries_per_item(g.n, g.n_cells)
-                    : gram ? kGramQueries
-                    : dmma ? tc_queries_per_item(g.d_pad, g.n, g.n_cells)
-                           : core_queries_per_item(g.d, g.d_pad);
-    // lowd: items never split a candidate list (each query row comes from one item);
-    // gram: 64-query items x 32k-candidate slices
-    const int64_t target = lowd   ? (int64_t(1) << 60)
-                           : gram ? int64_t(kGramQueries) * kGramSlice
-                                  : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
-    ctx->n_items = build_work_items(ctx, cell_begin, cell_end, qpi, target, s,
-                                    lowd ? &counters(ctx)->n_items : nullptr);
+    if (rp.lowd) ensure_masks(ctx, s);
+    ctx->n_items = build_work_items(ctx, cell_begin, cell_end, rp.qpi, rp.target, s,
+                                    rp.lowd ? &counters(ctx)->n_items : nullptr);
     TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
-    RefineArgs a{};
-    a.P = ctx->P.as<double>();
-    a.NRM = ctx->NRM.as<double>();
-    a.CN = ctx->CN.as<double>();
-    a.SFX = ctx->SFX.as<double>();
-    a.runs = ctx->runs.as<uint2>();
-    a.run_off = ctx->run_off.as<uint32_t>();
-    a.cell_runs = ctx->cell_runs.as<int64_t>();
-    a.cell_start = ctx->cell_start.as<int64_t>();
-    a.items = ctx->items.as<WorkItem>();
-    a.n_items = ctx->n_items;
-    a.n_items_dev = lowd ? &counters(ctx)->n_items : nullptr;
-    a.ctr = counters(ctx);
-    a.pairs = ctx->pairs.as<uint2>();
-    a.pair_cap = ctx->pair_cap;
-    a.qcount = ctx->qcount.as<uint32_t>();
-    a.masks = ctx->masks.as<unsigned long long>();
-    a.cell_mbase = ctx->cell_mbase.as<int64_t>();
-    a.cell_base = 0;
-    a.d = g.d;
-    a.d_pad = g.d_pad;
-    a.nchunks = g.nchunks;
-    a.eps_sq = g.eps_sq;
-    a.guard_rel = guard_rel(g.d, g.d_pad);
-    a.max_norm = g.max_norm + g.eps_sq;
-    a.short_circuit = short_circuit ? 1 : 0;
+    const RefineArgs a = refine_args(ctx, rp, short_circuit);
     TJ_CUDA(cudaEventRecord(ctx->ev0, s));
-    if (lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
-    else if (gram) launch_refine_gram(a, s);
-    else if (dmma) launch_refine_tc(a, g.n, g.n_cells, s);
-    else {
-      // CUDA-core variants (refine_core.cu): the expanded form needs finite norms
-      const int variant = kernel == TJ_KERNEL_CORE_FMA                   ? 1
-                          : kernel == TJ_KERNEL_CORE_EXPANDED && norms_ok ? 2
-                                                                          : 0;
-      launch_refine_core(a, variant, s);
-    }
+    launch_refine(ctx, rp, a, s);
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;
     // low-d rows are counted from the hit masks (pairs per query + total hits)
-    if (lowd)
+    if (rp.lowd)
       launch_count_rows(ctx, cell_begin, cell_end, &counters(ctx)->hits, &counters(ctx)->max_row, s);
+  });
+}
+
+__global__ void zero_sample_counts_kernel(const WorkItem* __restrict__ items, int64_t n_items,
+                                          uint32_t* __restrict__ qcount) {
+  for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x)
+    for (uint32_t q = threadIdx.x; q < items[i].nq; q += blockDim.x) qcount[items[i].q0 + q] = 0;
+}
+
+int tj_estimate_pairs(tj_ctx* ctx, int32_t kernel, int64_t cell_begin, int64_t cell_end,
+                      int32_t samples, uint64_t seed, double* pairs_per_candidate, void* stream) {
+  if (!ctx || !pairs_per_candidate) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    const GridState& g = ctx->g;
+    if (kernel < TJ_KERNEL_CORE || kernel > TJ_KERNEL_CORE_EXPANDED)
+      fail(TJ_EINVAL, "kernel must be one of TJ_KERNEL_CORE, _DMMA, _CORE_FMA, _CORE_EXPANDED");
+    if (cell_begin < 0 || cell_end > g.n_cells || cell_begin > cell_end || samples < 1)
+      fail(TJ_EINVAL, "need a valid cell range and samples >= 1");
+    *pairs_per_candidate = 0.0;
+    if (cell_begin == cell_end) return;
+    const RefinePlan rp = plan_refine(ctx, kernel);
+    if (rp.lowd) fail(TJ_EINVAL, "the low-d DMMA kernel records hit masks: nothing to size");
+    // sample items: cells drawn with probability |cell|*|cand| (the estimator),
+    // one query block at a random offset of the cell against its whole list
+    const int64_t nc = cell_end - cell_begin;
+    std::vector<int64_t> cost(nc), start(nc + 1), cand(nc);
+    TJ_CUDA(cudaStreamSynchronize(s));
+    TJ_CUDA(cudaMemcpy(cost.data(), ctx->cell_cost.as<int64_t>() + cell_begin, sizeof(int64_t) * nc,
+                       cudaMemcpyDeviceToHost));
+    TJ_CUDA(cudaMemcpy(start.data(), ctx->cell_start.as<int64_t>() + cell_begin,
+                       sizeof(int64_t) * (nc + 1), cudaMemcpyDeviceToHost));
+    TJ_CUDA(cudaMemcpy(cand.data(), ctx->cell_cand.as<int64_t>() + cell_begin, sizeof(int64_t) * nc,
+                       cudaMemcpyDeviceToHost));
+    std::vector<double> cum(nc + 1, 0.0);
+    for (int64_t c = 0; c < nc; ++c) cum[c + 1] = cum[c] + double(cost[c]);
+    if (cum[nc] <= 0) return;
+    uint64_t st = seed * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull;
+    auto next = [&]() {  // splitmix64
+      uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      return z ^ (z >> 31);
+    };
+    std::vector<WorkItem> items;
+    for (int i = 0; i < samples; ++i) {
+      const double u = double(next() >> 11) * 0x1.0p-53 * cum[nc];
+      const int64_t c = std::min<int64_t>(
+          nc - 1, std::upper_bound(cum.begin(), cum.end(), u) - cum.begin() - 1);
+      const int64_t sz = start[c + 1] - start[c];
+      if (sz <= 0 || cand[c] <= 0) continue;
+      const int64_t nq = std::min<int64_t>(rp.qpi, sz);
+      const int64_t q0 = start[c] + int64_t(next() % uint64_t(sz - nq + 1));
+      WorkItem w{};
+      w.cell = uint32_t(cell_begin + c);
+      w.q0 = uint32_t(q0);
+      w.nq = uint32_t(nq);
+      w.s0 = 0;
+      w.s1 = uint32_t(cand[c]);
+      items.push_back(w);
+    }
+    if (items.empty()) return;
+    // run them on the refine kernel, appends counted (not stored) past the buffer;
+    // the counters and the sampled queries' counts are restored afterwards
+    ctx->items.ensure(sizeof(WorkItem) * items.size(), s);
+    TJ_CUDA(cudaMemcpyAsync(ctx->items.ptr, items.data(), sizeof(WorkItem) * items.size(),
+                            cudaMemcpyHostToDevice, s));
+    ctx->n_items = int64_t(items.size());
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx) + 1, counters(ctx), sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+    DevCounters before{};
+    TJ_CUDA(cudaMemcpyAsync(&before, counters(ctx), sizeof(before), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaMemsetAsync(&counters(ctx)->item_next, 0, sizeof(unsigned long long), s));
+    RefineArgs a = refine_args(ctx, rp, 1);
+    a.pair_cap = std::min<unsigned long long>(ctx->pair_cap, before.pairs);  // store nothing new
+    launch_refine(ctx, rp, a, s);
+    DevCounters after{};
+    TJ_CUDA(cudaMemcpyAsync(&after, counters(ctx), sizeof(after), cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx), counters(ctx) + 1, sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+    zero_sample_counts_kernel<<<unsigned(std::min<size_t>(items.size(), 4096)), 64, 0, s>>>(
+        ctx->items.as<WorkItem>(), int64_t(items.size()), ctx->qcount.as<uint32_t>());
+    TJ_CHECK_LAUNCH();
+    TJ_CUDA(cudaStreamSynchronize(s));
+    ctx->ctr_valid = false;
+    const double refined = double(after.refined - before.refined);
+    *pairs_per_candidate = refined > 0 ? double(after.pairs - before.pairs) / refined : 0.0;
   });
 }
 

@@ -432,14 +432,16 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     if (__ballot_sync(0xffffffffu, len > 0) == 0u) continue;
     const uint32_t id = valid ? perm[p] : 0u;
     const int64_t dst = valid ? offsets[id] : 0;
-    int64_t c0, c;
+    int64_t c0, c, c_last;
     if constexpr (LIST) {  // positions ascend along the window: lane 0 has the first cell
-      c = valid ? int64_t(rl.pcell[p]) : -1;
-      c0 = __shfl_sync(0xffffffffu, c, 0);
-      if (!valid) c = c0;
+      const int cv = valid ? int(rl.pcell[p]) : -1;
+      c0 = __shfl_sync(0xffffffffu, cv, 0);
+      c_last = __reduce_max_sync(0xffffffffu, cv);  // the last valid lane's cell
+      c = valid ? cv : c0;
     } else {
       c0 = win_cell[w];
       c = window_lane_cell(cell_start, n_cells, c0, w << 5);
+      c_last = __shfl_sync(0xffffffffu, c, 31);
     }
     const bool pooled = len > 0 && len <= kPoolSlots;
     if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = uint32_t(p);
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
       for (int b = 0; b < mr.nblk; b += 4) prefetch_l1(mr.m + b);
     }
     // run tables + block hints of the window's first kEmitCells cells
-    const int ncw = int(min(__shfl_sync(0xffffffffu, c, 31) + 1, n_cells) - c0);
+    const int ncw = int(min(c_last + 1, n_cells) - c0);
     __syncwarp();
     for (int ci = 0; ci < min(ncw, kEmitCells); ++ci) {
       const int64_t rb = cell_runs[c0 + ci], nr = cell_runs[c0 + ci + 1] - rb;

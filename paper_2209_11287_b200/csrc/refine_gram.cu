@@ -47,6 +47,7 @@ struct GramSmem {
   double q[kGramQ][S::STRIDE];                   // -2 * query coordinates
   double c[kGramStages][kGramC][S::STRIDE];      // candidate coordinates
   double cn[kGramStages][kGramC];                // |c|^2 (padding rows: kPadNorm)
+  double thr[kGramQ], tlo[kGramQ];               // per query: guard band edges (see below)
   uint32_t pos[kGramStages][kGramC];             // cell-ordered positions
   uint2 hits[kGramWarps][kHitBuf];
 };
@@ -83,8 +84,8 @@ __device__ __noinline__ uint2 gram_recheck(const double* P, int dp, int d, doubl
   return make_uint2(__ballot_sync(0xffffffffu, p0), __ballot_sync(0xffffffffu, p1));
 }
 
-template <int NCH>
-__global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs a) {
+template <int NCH, int MINB>
+__global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineArgs a) {
   using S = GramShape<NCH>;
   constexpr int DP = S::DP, PPR = S::PPR;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -120,19 +121,15 @@ __global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs
       sm.q[r][2 * pc] = -2.0 * v.x;
       sm.q[r][2 * pc + 1] = -2.0 * v.y;
     }
-    // thresholds of this lane's 8 queries: 8*(4*wq + g) + 2*col + jj
-    double thr[4][2], tlo[4][2];
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int q = 32 * wq + 8 * g + 2 * col + jj;
-        const bool v = q < nq;
-        const double qn = v ? a.NRM[it.q0 + q] : 0.0;
-        const double guard = a.guard_rel * (qn + a.max_norm) + 1e-300;
-        thr[g][jj] = v ? eps_sq - qn + guard : -INFINITY;
-        tlo[g][jj] = v ? eps_sq - qn - guard : INFINITY;
-      }
+    // guard band edges per query (shared: registers go to the accumulators)
+    if (threadIdx.x < kGramQ) {
+      const int q = threadIdx.x;
+      const bool v = q < nq;
+      const double qn = v ? a.NRM[it.q0 + q] : 0.0;
+      const double guard = a.guard_rel * (qn + a.max_norm) + 1e-300;
+      sm.thr[q] = v ? eps_sq - qn + guard : -INFINITY;
+      sm.tlo[q] = v ? eps_sq - qn - guard : INFINITY;
+    }
     unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
     if (threadIdx.x == 0) st_tiles_ref += uint64_t((nq + 7) >> 3) * ((s1 - s0 + 7) >> 3);
 
@@ -183,7 +180,7 @@ __global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs
 #pragma unroll
         for (int g = 0; g < 4; ++g) acc[b][g][0] = acc[b][g][1] = cn;
       }
-#pragma unroll 4
+#pragma unroll 2
       for (int j = 0; j < NCH; ++j) {
         double av[4], bv[4];
 #pragma unroll
@@ -195,7 +192,14 @@ __global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs
 #pragma unroll
           for (int g = 0; g < 4; ++g) gram_mma(acc[b][g][0], acc[b][g][1], av[b], bv[g]);
       }
-      // epilogue: one branch per stage
+      // epilogue: one branch per stage; this lane's queries 32*wq + 8*g + 2*col + jj
+      double thr[4][2];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const double2 t = *reinterpret_cast<const double2*>(&sm.thr[32 * wq + 8 * g + 2 * col]);
+        thr[g][0] = t.x;
+        thr[g][1] = t.y;
+      }
       unsigned any = 0u;
 #pragma unroll
       for (int b = 0; b < 4; ++b)
@@ -215,8 +219,9 @@ __global__ void __launch_bounds__(kGramThreads, 2) refine_gram_kernel(RefineArgs
             unsigned m1 = __ballot_sync(0xffffffffu, p1);
             if ((m0 | m1) == 0) continue;
             const uint32_t qa = it.q0 + 32 * wq + 8 * g + 2 * col;
-            const bool b0 = p0 && acc[b][g][0] > tlo[g][0];
-            const bool b1 = p1 && acc[b][g][1] > tlo[g][1];
+            const double2 tl = *reinterpret_cast<const double2*>(&sm.tlo[32 * wq + 8 * g + 2 * col]);
+            const bool b0 = p0 && acc[b][g][0] > tl.x;
+            const bool b1 = p1 && acc[b][g][1] > tl.y;
             if (__any_sync(0xffffffffu, b0 || b1)) {
               const uint2 m = gram_recheck(a.P, DP, a.d, eps_sq, b0, b1, m0, m1, qa, cpos,
                                            &a.ctr->rechecks);
@@ -264,7 +269,9 @@ bool gram_applies(int d_pad, int64_t n, int64_t n_cells) {
 template <int NCH>
 static void launch_gram_t(const RefineArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(GramSmem<NCH>);
-  auto kern = refine_gram_kernel<NCH>;
+  // 3 CTAs (12 warps, <= 168 registers) per SM while the shared memory allows
+  constexpr int kMinBlocks = NCH <= 10 ? 3 : 2;
+  auto kern = refine_gram_kernel<NCH, kMinBlocks>;
   TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGramThreads, smem));

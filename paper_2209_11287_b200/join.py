@@ -336,8 +336,7 @@ class DeviceJoin:
         return plan_from_estimates(self.ctx.cell_costs(self.info.n_cells), self.config.batch_size)
 
     # ---- output-budget batcher (join.py:184-202) ----
-    SAMPLE_RANGES = 8          # contiguous cell ranges refined to estimate |R|
-    SAMPLE_SHARE = 1.0 / 256   # of the candidate pairs, per range
+    SAMPLE_ITEMS = 256         # query blocks refined to estimate |R| (tj_estimate_pairs)
     SAMPLE_ABOVE = 1 << 24     # candidate pairs below which the buffer is just sized to C
 
     def appends_pairs(self) -> bool:
@@ -346,39 +345,19 @@ class DeviceJoin:
         return not (self.kernel == _native.TJ_KERNEL_DMMA and self.work.d_padded == 4)
 
     def estimate_pairs(self, batches, costs=None) -> int:
-        """Result pairs of `batches`, estimated from a sampled refine: a few contiguous
-        cell ranges (each ~1/256 of the candidate pairs, spread over the batches) are
-        refined, their pair rate per candidate pair is extrapolated, +25% margin."""
+        """Result pairs of `batches` from a sampled selectivity: SAMPLE_ITEMS query
+        blocks of cost-weighted random cells run on the refine kernel with nothing
+        stored (tj_estimate_pairs); pairs per candidate pair x candidate pairs,
+        +25% and a floor for the sampling error."""
         if costs is None:
             costs = self.ctx.cell_costs(self.info.n_cells)
         csum = np.concatenate([[0], np.cumsum(costs)])
         total_c = int(sum(csum[b] - csum[a] for a, b in batches))
         if total_c <= self.SAMPLE_ABOVE:
             return total_c
-        # sample ranges: starting points evenly spaced in candidate-pair order
-        cells, sampled = [], 0
-        offsets = np.linspace(0, total_c, self.SAMPLE_RANGES + 2)[1:-1]
-        acc, flat = 0, []
-        for a, b in batches:
-            flat.append((a, b, acc))
-            acc += int(csum[b] - csum[a])
-        for off in offsets:
-            for a, b, base in flat:
-                if base <= off < base + (csum[b] - csum[a]):
-                    c0 = int(np.searchsorted(csum, csum[a] + (off - base), side="right")) - 1
-                    want = csum[c0] + max(int(total_c * self.SAMPLE_SHARE), 1)
-                    c1 = min(b, max(c0 + 1, int(np.searchsorted(csum, want, side="left"))))
-                    cells.append((c0, c1))
-                    sampled += int(csum[c1] - csum[c0])
-                    break
-        self.ctx.reset_results()
-        self.ctx.reserve_results(sampled)
-        for c0, c1 in cells:
-            self.ctx.refine(self.kernel, self.config.short_circuit, c0, c1)
-        hits, _ = self.ctx.result_count()
-        self.ctx.reset_results()
-        rate = hits / max(sampled, 1)
-        return int(min(total_c, rate * total_c * 1.25 + 4096))
+        lo, hi = min(a for a, _ in batches), max(b for _, b in batches)
+        rate = self.ctx.estimate_pairs(self.kernel, lo, hi, self.SAMPLE_ITEMS)
+        return int(min(total_c, rate * total_c * 1.25 + (1 << 20)))
 
     def refine(self, cell_range=None, max_result_pairs=None, plan=None):
         """Run every batch; returns the exact pair count.
