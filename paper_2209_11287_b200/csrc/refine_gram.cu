@@ -48,7 +48,7 @@ struct GramSmem {
   double c[kGramStages][kGramC][S::STRIDE];      // candidate coordinates
   double cn[kGramStages][kGramC];                // |c|^2 (padding rows: kPadNorm)
   double thr[kGramQ], tlo[kGramQ];               // per query: guard band edges (see below)
-  uint32_t pos[kGramStages][kGramC];             // cell-ordered positions
+  uint32_t pos[3][kGramC];                       // cell-ordered positions, by stage % 3
   uint2 hits[kGramWarps][kHitBuf];
 };
 
@@ -133,42 +133,52 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
     unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
     if (threadIdx.x == 0) st_tiles_ref += uint64_t((nq + 7) >> 3) * ((s1 - s0 + 7) >> 3);
 
-    // stage st: candidates s0 + 64 st + r; threads 0..63 map offsets to positions
-    auto issue = [&](int st) {
-      const int buf = st % kGramStages;
-      if (st < nst) {
-        if (threadIdx.x < kGramC) {
-          const uint32_t t = s0 + uint32_t(st) * kGramC + threadIdx.x;
-          uint32_t p = 0xffffffffu;
-          if (t < s1) {
-            int lo = 0, hi = nr;
-            while (hi - lo > 1) {
-              const int mid = (lo + hi) >> 1;
-              if (a.run_off[rb + mid] <= t) lo = mid;
-              else hi = mid;
-            }
-            p = a.runs[rb + lo].x + (t - a.run_off[rb + lo]);
+    // stage st: candidates s0 + 64 st + r.  Threads 0..63 map offsets to positions
+    // (slot st % 3: the epilogue of stage st - 1 may still read slot (st - 1) % 3)
+    auto map_positions = [&](int st) {
+      if (st < nst && threadIdx.x < kGramC) {
+        const uint32_t t = s0 + uint32_t(st) * kGramC + threadIdx.x;
+        uint32_t p = 0xffffffffu;
+        if (t < s1) {
+          int lo = 0, hi = nr;
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (a.run_off[rb + mid] <= t) lo = mid;
+            else hi = mid;
           }
-          sm.pos[buf][threadIdx.x] = p;
+          p = a.runs[rb + lo].x + (t - a.run_off[rb + lo]);
         }
-        __syncthreads();
+        sm.pos[st % 3][threadIdx.x] = p;
+      }
+    };
+    // cp.async of stage st into buffer st % 2 (its positions are visible)
+    auto issue = [&](int st) {
+      if (st < nst) {
+        const int buf = st % kGramStages;
+        const uint32_t* pos = sm.pos[st % 3];
         for (int i = threadIdx.x; i < kGramC * PPR; i += kGramThreads) {
           const int r = i / PPR, pc = i - r * PPR;
-          const uint32_t p = sm.pos[buf][r];
+          const uint32_t p = pos[r];
           if (p != 0xffffffffu) gram_cp16(&sm.c[buf][r][2 * pc], a.P + size_t(p) * DP + 2 * pc);
           else *reinterpret_cast<double2*>(&sm.c[buf][r][2 * pc]) = make_double2(0.0, 0.0);
         }
         if (threadIdx.x < kGramC) {
-          const uint32_t p = sm.pos[buf][threadIdx.x];
+          const uint32_t p = pos[threadIdx.x];
           if (p != 0xffffffffu) gram_cp8(&sm.cn[buf][threadIdx.x], a.NRM + p);
           else sm.cn[buf][threadIdx.x] = kPadNorm;
         }
       }
       gram_commit();
     };
+    map_positions(0);
+    __syncthreads();
     issue(0);
+    // two barriers per stage: (1) stage st+1's positions visible and every warp
+    // done with stage st-1 (its buffer is refilled next); (2) stage st landed
 #pragma unroll 1
     for (int st = 0; st < nst; ++st) {
+      map_positions(st + 1);
+      __syncthreads();
       issue(st + 1);
       gram_wait<1>();
       __syncthreads();
@@ -200,14 +210,14 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
         thr[g][0] = t.x;
         thr[g][1] = t.y;
       }
-      unsigned any = 0u;
+      // one predicate per lane (DSETP with OR-accumulate), one vote per stage
+      bool pass = false;
 #pragma unroll
       for (int b = 0; b < 4; ++b)
 #pragma unroll
         for (int g = 0; g < 4; ++g)
-          any |= __ballot_sync(0xffffffffu, acc[b][g][0] <= thr[g][0]) |
-                 __ballot_sync(0xffffffffu, acc[b][g][1] <= thr[g][1]);
-      if (any) {
+          pass = pass || (acc[b][g][0] <= thr[g][0]) || (acc[b][g][1] <= thr[g][1]);
+      if (__any_sync(0xffffffffu, pass)) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t cpos = sm.pos[buf][32 * wc + 8 * b + row];
@@ -240,7 +250,6 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
           }
         }
       }
-      __syncthreads();  // stage buffer `buf` is refilled by issue(st + 2)
     }
     gram_wait<0>();
     // per-query counts (items of one cell share queries across slices: atomics)

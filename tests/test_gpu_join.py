@@ -490,12 +490,18 @@ def test_small_join_then_large_batched_join_with_cap():
 
 
 def test_pair_estimate_is_close_for_uniform_data():
+    """tj_estimate_pairs (sampled, nothing stored) brackets the exact count: the buffer
+    it sizes holds the result without a re-run and without gross over-allocation."""
     from paper_2209_11287_b200.join import DeviceJoin
 
-    ds = generate(GenSpec("uniform", 200_000, 6, seed=4))
-    eps = 0.08
-    job = DeviceJoin(ds, JoinConfig(epsilon=eps, kernel="scalar"))
-    job.build()
-    est = job.estimate_pairs([(0, job.info.n_cells)])
-    total = job.refine()
-    assert total <= est <= 2 * total
+    for kernel, (n, d, eps) in (("scalar", (1_000_000, 4, 0.065)), ("tile", (600_000, 8, 0.3)),
+                                ("core_fma", (1_000_000, 4, 0.065))):
+        ds = generate(GenSpec("uniform", n, d, seed=4))
+        job = DeviceJoin(ds, JoinConfig(epsilon=eps, kernel=kernel))
+        job.build()
+        assert job.info.candidates > DeviceJoin.SAMPLE_ABOVE
+        est = job.estimate_pairs([(0, job.info.n_cells)])
+        total = job.refine()
+        assert total <= est <= 2 * total, (kernel, total, est)
+        r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
+        assert r.total_pairs == total

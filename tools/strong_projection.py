@@ -1,0 +1,118 @@
+"""Per-rank device time of the strong multi-GPU layout, measured on ONE GPU.
+
+    python tools/strong_projection.py [config] [G ...]
+
+For G ranks, every rank's step (distributed.strong_self_join without the
+collectives: halo select, local grid, refine of the owned cells, canonical rows,
+id remap, count scatter, global offsets) is run in turn on this device with CUDA
+events; the step time of G GPUs is the slowest rank plus the collectives,
+estimated from their byte counts at a stated NVLink bus bandwidth.  Efficiency
+= T_1 / (G * T_G).  This is a projection (one GPU measures each rank's share);
+the collectives are not measured here.
+"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np
+import torch
+
+from bench import CONFIGS
+from paper_2209_11287_b200 import GenSpec, JoinConfig, _native, generate
+from paper_2209_11287_b200.datasets import Dataset
+from paper_2209_11287_b200.distributed import plan_bins, prefix_dims
+from paper_2209_11287_b200.join import DeviceJoin
+
+NVLINK_BUS_GBS = 500.0  # assumed NCCL bus bandwidth per GPU (B200 NVLink 5: 900 GB/s per direction)
+
+name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].isdigit() else "c5"
+Gs = [int(a) for a in sys.argv[1:] if a.isdigit()] or [1, 2, 4, 8]
+dist, n, d, eps = CONFIGS[name]
+ds = generate(GenSpec(dist, n, d, seed=0))
+dev = "cuda:0"
+coords = torch.from_numpy(ds.coords).to(dev)
+cfg = JoinConfig(epsilon=eps)
+ctx = _native.context(0)
+pdims = prefix_dims(d, min(d, 6))
+
+
+def ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def full_join():
+    t = [ev()]
+    job = DeviceJoin(ds, cfg)
+    job.build(coords)
+    t.append(ev())
+    job.refine()
+    t.append(ev())
+    job.finalize()
+    t.append(ev())
+    torch.cuda.synchronize()
+    del job
+    return [t[i].elapsed_time(t[i + 1]) for i in range(3)]
+
+
+for _ in range(2):
+    full_join()
+T1 = float(np.median([sum(full_join()) for _ in range(3)]))
+lo, hi = ctx.shard_bounds(coords, n, pdims, eps)
+origin = lo
+span = (int(hi[0] - lo[0] + 1), int(hi[1] - lo[1] + 1) if pdims > 1 else 1)
+hist = torch.zeros(span[0] * span[1], dtype=torch.int64, device=dev)
+ctx.shard_histogram(coords, n, pdims, eps, origin, span, hist)
+h = hist.cpu().numpy()
+
+
+def rank_step(plan, r):
+    lo_b, hi_b = plan.owned(r)
+    t = [ev()]
+    n_local = ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b)
+    local = torch.empty((max(n_local, 1), coords.shape[1]), dtype=torch.float64, device=dev)
+    gid = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
+    ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b, out=local, gid=gid)
+    t.append(ev())
+    job = DeviceJoin(Dataset._wrap(np.empty((n_local, coords.shape[1])), d), cfg)
+    job.build(local[:n_local])
+    cb, ce = ctx.shard_cell_range(pdims, plan.origin, plan.span, lo_b, hi_b)
+    t.append(ev())
+    pairs = job.refine(cell_range=(cb, ce))
+    t.append(ev())
+    loff, lnbr = job.finalize()
+    ctx.remap_ids(lnbr, pairs, gid)
+    counts = torch.zeros(n, dtype=torch.int32, device=dev)
+    ctx.scatter_counts(loff, n_local, gid, counts)
+    goff = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ctx.counts_to_offsets(counts, n, goff)
+    t.append(ev())
+    torch.cuda.synchronize()
+    ph = [t[i].elapsed_time(t[i + 1]) for i in range(4)]
+    return {"rank": r, "n_local": n_local, "pairs": pairs, "select_ms": ph[0], "index_ms": ph[1],
+            "refine_ms": ph[2], "output_ms": ph[3], "step_ms": sum(ph)}
+
+
+out = {"config": name, "n": n, "d": d, "T1_ms": T1, "nvlink_bus_gbs_assumed": NVLINK_BUS_GBS,
+       "projection": []}
+for G in Gs:
+    if G == 1:
+        continue
+    plan = plan_bins(h, pdims, origin, span, G)
+    ranks = [rank_step(plan, r) for r in range(G)]
+    ranks = [rank_step(plan, r) for r in range(G)]  # second pass: warm allocator
+    worst = max(ranks, key=lambda x: x["step_ms"])
+    coll_bytes = {"all_gather_coords": (G - 1) / G * n * coords.shape[1] * 8,
+                  "all_reduce_counts": 2 * (G - 1) / G * n * 4}
+    coll_ms = sum(b / (NVLINK_BUS_GBS * 1e9) * 1e3 for b in coll_bytes.values())
+    TG = worst["step_ms"] + coll_ms
+    row = {"G": G, "slowest_rank": worst, "mean_rank_ms": float(np.mean([x["step_ms"] for x in ranks])),
+           "collectives_ms_est": coll_ms, "T_G_ms": TG, "efficiency": T1 / (G * TG),
+           "efficiency_device_only": T1 / (G * worst["step_ms"]),
+           "pairs_total": int(sum(x["pairs"] for x in ranks))}
+    out["projection"].append(row)
+    print(json.dumps(row), flush=True)
+print(json.dumps(out))
