@@ -133,22 +133,35 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
     unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
     if (threadIdx.x == 0) st_tiles_ref += uint64_t((nq + 7) >> 3) * ((s1 - s0 + 7) >> 3);
 
-    // stage st: candidates s0 + 64 st + r.  Threads 0..63 map offsets to positions
-    // (slot st % 3: the epilogue of stage st - 1 may still read slot (st - 1) % 3)
+    // stage st: candidates s0 + 64 st + r.  Thread r < 64 follows offsets
+    // s0 + r, s0 + r + 64, ... through the cell's runs with a cursor (one binary
+    // search per item; per stage a compare, a load only when a run ends), and
+    // writes slot st % 3 (the epilogue of stage st - 1 may still read its slot).
+    int rk = 0;
+    uint32_t r_off = 0, r_pos = 0, r_end = 0xffffffffu;
+    if (threadIdx.x < kGramC) {
+      const uint32_t t0 = s0 + threadIdx.x;
+      int lo = 0, hi = nr;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.run_off[rb + mid] <= t0) lo = mid;
+        else hi = mid;
+      }
+      rk = lo;
+      r_off = a.run_off[rb + rk];
+      r_pos = a.runs[rb + rk].x;
+      r_end = rk + 1 < nr ? a.run_off[rb + rk + 1] : 0xffffffffu;
+    }
     auto map_positions = [&](int st) {
       if (st < nst && threadIdx.x < kGramC) {
         const uint32_t t = s0 + uint32_t(st) * kGramC + threadIdx.x;
-        uint32_t p = 0xffffffffu;
-        if (t < s1) {
-          int lo = 0, hi = nr;
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (a.run_off[rb + mid] <= t) lo = mid;
-            else hi = mid;
-          }
-          p = a.runs[rb + lo].x + (t - a.run_off[rb + lo]);
+        while (t >= r_end) {
+          ++rk;
+          r_off = r_end;
+          r_pos = a.runs[rb + rk].x;
+          r_end = rk + 1 < nr ? a.run_off[rb + rk + 1] : 0xffffffffu;
         }
-        sm.pos[st % 3][threadIdx.x] = p;
+        sm.pos[st % 3][threadIdx.x] = t < s1 ? r_pos + (t - r_off) : 0xffffffffu;
       }
     };
     // cp.async of stage st into buffer st % 2 (its positions are visible)
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
       if (__any_sync(0xffffffffu, pass)) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const uint32_t cpos = sm.pos[buf][32 * wc + 8 * b + row];
+          const uint32_t cpos = sm.pos[st % 3][32 * wc + 8 * b + row];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const bool p0 = acc[b][g][0] <= thr[g][0];
