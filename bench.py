@@ -14,8 +14,9 @@ the measurement through the public API `self_join(host Dataset, JoinConfig)`
 with H2D of the coordinates and D2H of the CSR pair set inside the timed
 region.  N>1 ranks (torchrun) default to config 5 strong-scaled: each rank
 holds a 1/N row slice, the step plans equal-cost bin ranges (NCCL all-reduces),
-all-gathers the coordinates, joins its bins' cells and all-reduces the per-id
-counts into the global offsets (distributed.py); times are the max over ranks.
+routes every rank's bins + halo points to it (one all-to-all), joins its bins'
+cells and all-reduces the per-id counts into the global offsets
+(distributed.py); times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -615,8 +616,8 @@ def run_ours(args, world, rank, local):
 def run_strong(args, world, rank, local):
     """N > 1, strong scaling (the default): ONE workload (config 5 unless --config)
     split by estimated cost over the ranks with the strong layout of
-    distributed.py -- every step all-reduces the bin bounds/histogram, all-gathers
-    the coordinates (NCCL), selects each rank's bins + halo on the device, builds
+    distributed.py -- every step all-reduces the bin bounds/histogram, routes every
+    rank's rows to the ranks needing them (one NCCL all-to-all: bins + halo), builds
     the local grid, refines the owned cells, emits canonical rows and all-reduces
     the per-id counts into the global CSR offsets.  Inputs at step start: each
     rank's 1/N row slice resident on its device.  Times are CUDA events on each
@@ -645,7 +646,7 @@ def run_strong(args, world, rank, local):
                      device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream(dev)
-    phases = ("plan", "gather", "select", "index", "refine", "offsets")
+    phases = ("plan", "exchange", "index", "refine", "offsets")
 
     def one_step(timings=None):
         evs = {"start": torch.cuda.Event(enable_timing=True)}
@@ -732,7 +733,7 @@ def run_strong(args, world, rank, local):
         "workload_stats": {"candidate_pairs": C, "result_pairs": total,
                            "layout": f"{world} ranks own equal-cost contiguous (x0, x1) bin "
                                      "ranges; NCCL all-reduce of bounds, histogram and per-id "
-                                     "counts + all-gather of the coordinates inside the step"},
+                                     "counts + all-to-all of each rank's bins + halo points inside the step"},
         "phases_ms_max_over_ranks": phase_max,
         "rank0": {"n_local": timings[0]["n_local"], "pairs": timings[0]["rank_pairs"],
                   "refine_kernel_ms": ref_ms},

@@ -11,9 +11,11 @@ batch's cells (join.py:184-197) -- with the strong layout of SURVEY.md 8(e):
    3x3 neighbourhood count (the reference estimator |cell| * |cand(cell)|,
    join.py:122-124, at bin granularity), cut into G contiguous lexicographic
    bin ranges of equal cost -- contiguous cell ranges of the reference order;
-4. one all-gather of the coordinates (NCCL over NVLink), then each rank keeps
-   (stable compaction on the device, tj_shard_select) only its own bins' points
-   plus the one-cell halo its cells' candidate lists need;
+4. every rank routes its own rows to the ranks that need them -- a point goes to
+   the owner of its bin and to the ranks whose bins are in its one-cell halo
+   (stable compaction per destination on the device, tj_shard_select) -- and
+   one all-to-all (NCCL over NVLink) delivers each rank its bins' points plus
+   its halo, in global id order;
 5. each rank builds the grid over those points, refines only its owned cells
    (tj_shard_cell_range) and emits its canonical CSR rows; local ids are
    monotone in global ids, so rows stay sorted after tj_remap_ids;
@@ -184,6 +186,55 @@ class ShardResult:
     times: dict = field(default_factory=dict)
 
 
+def _a2a(out, inp, out_splits, in_splits, group):
+    """all_to_all_single; the gloo backend moves CUDA tensors through host memory."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "gloo" and inp.is_cuda:
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    return out
+
+
+def exchange_points(ctx, rows, gid_base: int, d: int, eps: float, plan: ShardPlan, group=None):
+    """Step 4: route this rank's rows (global ids gid_base + i) to every rank that needs
+    them and receive this rank's bins + halo.  Returns (coords (n_local, d_pad) f64,
+    gid int32 [n_local], n_local); rows come in global id order (sources are ordered
+    by id range, each source's rows stay in order)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n_my, width = rows.shape[0], rows.shape[1]
+    pdims = plan.pdims
+    counts = [ctx.shard_select(rows, n_my, d, pdims, eps, plan.origin, plan.span, lo, hi)
+              if n_my else 0 for lo, hi in plan.ranges]
+    total = sum(counts)
+    dev = rows.device
+    send = torch.empty((max(total, 1), width), dtype=torch.float64, device=dev)
+    send_gid = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    off = 0
+    for (lo, hi), c in zip(plan.ranges, counts):
+        if c:
+            ctx.shard_select(rows, n_my, d, pdims, eps, plan.origin, plan.span, lo, hi,
+                             out=send[off: off + c], gid=send_gid[off: off + c], gid_base=gid_base)
+        off += c
+    cdev = dev if dist.get_backend(group) != "gloo" else torch.device("cpu")
+    sc = torch.tensor(counts, dtype=torch.int64, device=cdev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(v) for v in rc.cpu().tolist()]
+    n_local = sum(recv_counts)
+    local = torch.empty((max(n_local, 1), width), dtype=torch.float64, device=dev)
+    gid = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
+    _a2a(local[:n_local], send[:total], recv_counts, counts, group)
+    _a2a(gid[:n_local], send_gid[:total], recv_counts, counts, group)
+    return local, gid, n_local
+
+
 def gather_rows(rows, n: int, group=None):
     """All-gather the ranks' row slices into the full (n, d_pad) coordinates (NCCL)."""
     import torch
@@ -217,7 +268,7 @@ def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> Sh
     """The strong layout's join step over the process group (steps 2-6 above).
 
     rows: this rank's slice of the input (device tensor, (len, d_pad) f64, rows
-    row_slice(n, rank, world)).  `timer(name)` (optional) is called at phase
+    row_slice(n, rank, world) -- the id order the exchange relies on).  `timer(name)` (optional) is called at phase
     boundaries (the bench records CUDA events there).
     """
     import torch
@@ -237,15 +288,10 @@ def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> Sh
     ctx = _native.context(dev.index)
     plan = plan_shards(ctx, rows, eps, pdims, group)
     mark("plan")
-    full = gather_rows(rows, n, group)
-    mark("gather")
+    a, _ = row_slice(n, rank, dist.get_world_size(group))
+    local, gid, n_local = exchange_points(ctx, rows, a, d, eps, plan, group)
+    mark("exchange")
     lo, hi = plan.owned(rank)
-    n_local = ctx.shard_select(full, n, d, pdims, eps, plan.origin, plan.span, lo, hi)
-    local = torch.empty((max(n_local, 1), rows.shape[1]), dtype=torch.float64, device=dev)
-    gid = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
-    ctx.shard_select(full, n, d, pdims, eps, plan.origin, plan.span, lo, hi, out=local, gid=gid)
-    del full
-    mark("select")
     work = Dataset._wrap(np.empty((max(n_local, 1), rows.shape[1])), d) if n_local else work_shape
     job = DeviceJoin(work, config, device=dev.index)
     pairs = 0

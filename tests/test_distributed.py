@@ -104,16 +104,24 @@ def _strong_worker(rank, world, port, eps, shm_path, out_q):
         dist.all_reduce(hist, op=dist.ReduceOp.SUM)
         plan = plan_bins(hist.numpy(), pdims, origin, span, world)
         lo, hi = plan.owned(rank)
-        full = [torch.zeros((row_slice(n, 0, world)[1], rows.shape[1]), dtype=torch.float64)
-                for _ in range(world)]
-        mine = torch.zeros_like(full[0])
-        mine[: len(rows)] = torch.from_numpy(rows)
-        dist.all_gather(full, mine)
-        allx = torch.cat(full)[:n].numpy()
-        fb0, fb1 = point_bins(allx, eps, pdims, origin)
-        keep = halo_mask(fb0, fb1, span, pdims, lo, hi)
-        gid = np.flatnonzero(keep)  # stable: local ids monotone in global ids
-        local = np.ascontiguousarray(allx[keep])
+        # route this rank's rows to every rank needing them, one all-to-all
+        rb0, rb1 = point_bins(rows, eps, pdims, origin)
+        sends, send_gids, counts = [], [], []
+        for (olo, ohi) in plan.ranges:
+            m = halo_mask(rb0, rb1, span, pdims, olo, ohi)
+            sends.append(rows[m])
+            send_gids.append(a + np.flatnonzero(m))
+            counts.append(int(m.sum()))
+        rc = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rc, torch.tensor(counts, dtype=torch.int64))
+        rcounts = rc.tolist()
+        recv = torch.empty((sum(rcounts), rows.shape[1]), dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(np.concatenate(sends)), rcounts, counts)
+        rgid = torch.empty(sum(rcounts), dtype=torch.int64)
+        dist.all_to_all_single(rgid, torch.from_numpy(np.concatenate(send_gids)), rcounts, counts)
+        gid = rgid.numpy()
+        assert np.all(np.diff(gid) > 0)  # global id order: local ids monotone in global ids
+        local = np.ascontiguousarray(recv.numpy())
         _, cstart, ccoord, _ = oracle.grid(local, eps)
         cell_bin = (ccoord[:, 0] - origin[0]) * span[1] + (ccoord[:, 1] - origin[1])
         owned = np.flatnonzero((cell_bin >= lo) & (cell_bin <= hi))

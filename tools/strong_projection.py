@@ -3,8 +3,9 @@
     python tools/strong_projection.py [config] [G ...]
 
 For G ranks, every rank's step (distributed.strong_self_join without the
-collectives: halo select, local grid, refine of the owned cells, canonical rows,
-id remap, count scatter, global offsets) is run in turn on this device with CUDA
+collectives: routing of its row slice, local grid over its bins + halo, refine
+of the owned cells, canonical rows, id remap, count scatter, global offsets) is
+run in turn on this device with CUDA
 events; the step time of G GPUs is the slowest rank plus the collectives,
 estimated from their byte counts at a stated NVLink bus bandwidth.  Efficiency
 = T_1 / (G * T_G).  This is a projection (one GPU measures each rank's share);
@@ -69,13 +70,31 @@ ctx.shard_histogram(coords, n, pdims, eps, origin, span, hist)
 h = hist.cpu().numpy()
 
 
-def rank_step(plan, r):
+def rank_step(plan, r, G):
     lo_b, hi_b = plan.owned(r)
+    # exchange, this rank's side: route its own row slice to every rank (G selects);
+    # the all-to-all itself is estimated from the bytes received
+    per = -(-n // G)
+    sl = coords[r * per: min(n, (r + 1) * per)]
     t = [ev()]
+    cnts = [ctx.shard_select(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, a_, b_)
+            for a_, b_ in plan.ranges]
+    send = torch.empty((max(sum(cnts), 1), coords.shape[1]), dtype=torch.float64, device=dev)
+    sgid = torch.empty(max(sum(cnts), 1), dtype=torch.int32, device=dev)
+    off = 0
+    for (a_, b_), c_ in zip(plan.ranges, cnts):
+        if c_:
+            ctx.shard_select(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, a_, b_,
+                             out=send[off: off + c_], gid=sgid[off: off + c_], gid_base=r * per)
+        off += c_
+    t.append(ev())
+    # what this rank receives (the same set, in global id order)
     n_local = ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b)
     local = torch.empty((max(n_local, 1), coords.shape[1]), dtype=torch.float64, device=dev)
     gid = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
     ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b, out=local, gid=gid)
+    torch.cuda.synchronize()
+    t.append(ev())
     t.append(ev())
     job = DeviceJoin(Dataset._wrap(np.empty((n_local, coords.shape[1])), d), cfg)
     job.build(local[:n_local])
@@ -91,9 +110,10 @@ def rank_step(plan, r):
     ctx.counts_to_offsets(counts, n, goff)
     t.append(ev())
     torch.cuda.synchronize()
-    ph = [t[i].elapsed_time(t[i + 1]) for i in range(4)]
-    return {"rank": r, "n_local": n_local, "pairs": pairs, "select_ms": ph[0], "index_ms": ph[1],
-            "refine_ms": ph[2], "output_ms": ph[3], "step_ms": sum(ph)}
+    ph = [t[i].elapsed_time(t[i + 1]) for i in range(5)]
+    return {"rank": r, "n_local": n_local, "pairs": pairs, "route_ms": ph[0], "index_ms": ph[2],
+            "refine_ms": ph[3], "output_ms": ph[4], "step_ms": ph[0] + ph[2] + ph[3] + ph[4],
+            "recv_bytes": n_local * (coords.shape[1] * 8 + 4)}
 
 
 out = {"config": name, "n": n, "d": d, "T1_ms": T1, "nvlink_bus_gbs_assumed": NVLINK_BUS_GBS,
@@ -102,10 +122,10 @@ for G in Gs:
     if G == 1:
         continue
     plan = plan_bins(h, pdims, origin, span, G)
-    ranks = [rank_step(plan, r) for r in range(G)]
-    ranks = [rank_step(plan, r) for r in range(G)]  # second pass: warm allocator
+    ranks = [rank_step(plan, r, G) for r in range(G)]
+    ranks = [rank_step(plan, r, G) for r in range(G)]  # second pass: warm allocator
     worst = max(ranks, key=lambda x: x["step_ms"])
-    coll_bytes = {"all_gather_coords": (G - 1) / G * n * coords.shape[1] * 8,
+    coll_bytes = {"all_to_all_points": (G - 1) / G * worst["recv_bytes"],
                   "all_reduce_counts": 2 * (G - 1) / G * n * 4}
     coll_ms = sum(b / (NVLINK_BUS_GBS * 1e9) * 1e3 for b in coll_bytes.values())
     TG = worst["step_ms"] + coll_ms
