@@ -88,6 +88,7 @@ template <int NCH, int MINB>
 __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineArgs a) {
   using S = GramShape<NCH>;
   constexpr int DP = S::DP, PPR = S::PPR;
+  constexpr int kUnroll = NCH >= 8 ? 4 : 2;  // chunks whose fragment loads are hoisted together
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GramSmem<NCH>& sm = *reinterpret_cast<GramSmem<NCH>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
 #pragma unroll
         for (int g = 0; g < 4; ++g) acc[b][g][0] = acc[b][g][1] = cn;
       }
-#pragma unroll 2
+#pragma unroll(kUnroll)
       for (int j = 0; j < NCH; ++j) {
         double av[4], bv[4];
 #pragma unroll
@@ -223,14 +224,15 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
         thr[g][0] = t.x;
         thr[g][1] = t.y;
       }
-      // one predicate per lane (DSETP with OR-accumulate), one vote per stage
-      bool pass = false;
+      // one predicate per lane (DSETP with OR-accumulate, four independent chains
+      // so their latencies overlap), one vote per stage
+      bool pb[4] = {false, false, false, false};
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int g = 0; g < 4; ++g)
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          pass = pass || (acc[b][g][0] <= thr[g][0]) || (acc[b][g][1] <= thr[g][1]);
-      if (__any_sync(0xffffffffu, pass)) {
+        for (int b = 0; b < 4; ++b)
+          pb[b] = pb[b] || (acc[b][g][0] <= thr[g][0]) || (acc[b][g][1] <= thr[g][1]);
+      if (__any_sync(0xffffffffu, (pb[0] || pb[1]) || (pb[2] || pb[3]))) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t cpos = sm.pos[st % 3][32 * wc + 8 * b + row];
