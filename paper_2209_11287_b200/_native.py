@@ -54,6 +54,7 @@ SIGNATURES = {
     "tj_reset_results": (_i32, [_vp, _vp]),
     "tj_reserve_results": (_i32, [_vp, _i64]),
     "tj_checkpoint_results": (_i32, [_vp, _vp]),
+    "tj_set_symmetric": (_i32, [_vp, _i32]),
     "tj_estimate_pairs": (_i32, [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64,
                                  ctypes.POINTER(_f64), _vp]),
     "tj_rollback_results": (_i32, [_vp, _i64, _i64, _vp]),
@@ -209,6 +210,9 @@ class Context:
                                                int(cell_end), int(samples), int(seed),
                                                ctypes.byref(rate), s.cuda_stream))
         return float(rate.value)
+
+    def set_symmetric(self, on: bool):
+        self._check(self.lib.tj_set_symmetric(self.handle, int(bool(on))))
 
     def checkpoint_results(self, stream=None):
         s = stream or self.stream()

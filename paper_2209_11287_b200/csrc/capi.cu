@@ -3,6 +3,7 @@
 // the message for tj_last_error(); no C++ exception crosses the ABI.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.cuh"
@@ -61,6 +62,7 @@ static void zero_results(tj_ctx* ctx, cudaStream_t s) {
 // Dense hit-mask layout over all cells (low-d path); depends only on the grid.
 static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
   if (ctx->masks_ready) return;
+  if (ctx->symmetric) build_symmetric_tables(ctx, s);
   build_mask_bases(ctx, 0, ctx->g.n_cells, s);
   ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(ctx->g.tiles, 1), s);
   build_window_cells(ctx, s);
@@ -121,6 +123,8 @@ int tj_ctx_create(int device, tj_ctx** out) {
     TJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     tj_ctx* c = new tj_ctx();
     c->device = device;
+    const char* sym = std::getenv("TJ_SYMMETRIC");  // low-d symmetric join (default on)
+    c->symmetric = !(sym && sym[0] == '0');
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
     cudaEventCreate(&c->ev2);
@@ -139,7 +143,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
                     &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
                     &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
-                    &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell};
+                    &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell,
+                    &ctx->fwd,      &ctx->bt_start,  &ctx->bt,       &ctx->chunk_key};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -356,6 +361,7 @@ static RefineArgs refine_args(tj_ctx* ctx, const RefinePlan& rp, int32_t short_c
   a.masks = ctx->masks.as<unsigned long long>();
   a.cell_mbase = ctx->cell_mbase.as<int64_t>();
   a.cell_base = 0;
+  a.fwd = rp.lowd && ctx->symmetric ? ctx->fwd.as<uint32_t>() : nullptr;
   a.d = g.d;
   a.d_pad = g.d_pad;
   a.nchunks = g.nchunks;
@@ -496,6 +502,17 @@ int tj_estimate_pairs(tj_ctx* ctx, int32_t kernel, int64_t cell_begin, int64_t c
     ctx->ctr_valid = false;
     const double refined = double(after.refined - before.refined);
     *pairs_per_candidate = refined > 0 ? double(after.pairs - before.pairs) / refined : 0.0;
+  });
+}
+
+int tj_set_symmetric(tj_ctx* ctx, int32_t on) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    const bool want = on != 0;
+    if (want != ctx->symmetric) {
+      ctx->symmetric = want;
+      ctx->masks_ready = false;  // the mask layout depends on the mode
+    }
   });
 }
 

@@ -287,22 +287,95 @@ __device__ __forceinline__ int64_t window_lane_cell(const int64_t* __restrict__ 
   return c0 + __popc(starts & upto) - int(starts & 1u);
 }
 
+// Symmetric join tables (build_symmetric_tables); fwd == nullptr: plain join.
+struct SymTables {
+  const uint32_t* fwd;       // per cell: list offset of the cell's own first point
+  const int64_t* bt_start;   // per cell: backward entries [bt_start[c], bt_start[c+1])
+  const uint2* bt;           // (cell X < c, offset of c's first point in X's refined suffix)
+};
+
 struct MaskRow {
   const unsigned long long* m;  // the row's group: nblk masks
   int nblk;
   int shift;                    // 32 * (col & 1) + col / 2
+  uint32_t fwd;                 // list offset of block 0 (symmetric join), else 0
 };
 
 __device__ __forceinline__ MaskRow mask_row(const unsigned long long* __restrict__ masks,
                                             const int64_t* __restrict__ cell_mbase,
                                             const int64_t* __restrict__ cell_cand, int64_t c,
-                                            int64_t rel) {
+                                            int64_t rel, const uint32_t* __restrict__ fwd) {
   MaskRow r;
-  r.nblk = int((cell_cand[c] + 7) >> 3);
+  r.fwd = fwd ? fwd[c] : 0u;
+  r.nblk = int((cell_cand[c] - r.fwd + 7) >> 3);
   r.m = masks + cell_mbase[c] + (rel >> 3) * r.nblk;
   const int col = int(rel & 7);
   r.shift = 32 * (col & 1) + (col >> 1);
   return r;
+}
+
+// The 8 query bits of candidate row r of a tile mask: bit j < 4 -> query 2j,
+// bit 4 + j -> query 2j + 1 (the layout of refine_lowd.cu's ballots).
+__device__ __forceinline__ unsigned cand_row_bits(unsigned long long m, int r) {
+  return unsigned((m >> (4 * r)) & 0xFu) | (unsigned((m >> (32 + 4 * r)) & 0xFu) << 4);
+}
+
+// Backward part of a row (symmetric join): the point at offset `rel` of cell c
+// is a candidate of every earlier neighbour cell X; its pairs with X's queries
+// are candidate row (off & 7) of block (off >> 3) in each of X's query groups.
+template <class F>
+__device__ __forceinline__ void for_backward_hits(const SymTables& sym,
+                                                  const unsigned long long* __restrict__ masks,
+                                                  const int64_t* __restrict__ cell_mbase,
+                                                  const int64_t* __restrict__ cell_start,
+                                                  const int64_t* __restrict__ cell_cand,
+                                                  int64_t c, uint32_t rel, F&& f) {
+  const int64_t e1 = sym.bt_start[c + 1];
+  for (int64_t e = sym.bt_start[c]; e < e1; ++e) {
+    const uint2 xo = sym.bt[e];
+    const int64_t x = xo.x;
+    const uint32_t off = xo.y + rel;
+    const int64_t xs = cell_start[x];
+    const int ngx = int((cell_start[x + 1] - xs + 7) >> 3);
+    const int nblkx = int((cell_cand[x] - sym.fwd[x] + 7) >> 3);
+    const unsigned long long* m = masks + cell_mbase[x] + (off >> 3);
+    const int r = int(off & 7);
+    for (int g = 0; g < ngx; ++g) f(cand_row_bits(__ldg(m + int64_t(g) * nblkx), r), xs + 8 * g);
+  }
+}
+
+__device__ __forceinline__ int backward_count(const SymTables& sym,
+                                              const unsigned long long* __restrict__ masks,
+                                              const int64_t* __restrict__ cell_mbase,
+                                              const int64_t* __restrict__ cell_start,
+                                              const int64_t* __restrict__ cell_cand, int64_t c,
+                                              uint32_t rel) {
+  int cnt = 0;
+  for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c, rel,
+                    [&](unsigned bits, int64_t) { cnt += __popc(bits); });
+  return cnt;
+}
+
+// Query column of bit j of cand_row_bits: bits 0..3 -> 0, 2, 4, 6; 4..7 -> 1, 3, 5, 7.
+__device__ __forceinline__ int cand_bit_query(int j) { return j < 4 ? 2 * j : 2 * (j - 4) + 1; }
+
+// Original ids of a row's backward hits into its pool column from `slot` on.
+__device__ __noinline__ void emit_backward(const SymTables& sym,
+                                           const unsigned long long* __restrict__ masks,
+                                           const int64_t* __restrict__ cell_mbase,
+                                           const int64_t* __restrict__ cell_start,
+                                           const int64_t* __restrict__ cell_cand,
+                                           const uint32_t* __restrict__ perm, int64_t c,
+                                           uint32_t rel, uint32_t* col, int slot) {
+  for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c, rel,
+                    [&](unsigned bits, int64_t qbase) {
+                      while (bits) {
+                        const int j = __ffs(bits) - 1;
+                        bits &= bits - 1u;
+                        col[slot * kPoolLd] = __ldg(perm + qbase + cand_bit_query(j));
+                        ++slot;
+                      }
+                    });
 }
 
 __device__ __forceinline__ unsigned row_bits(unsigned long long m, int shift) {
@@ -316,7 +389,7 @@ __global__ void __launch_bounds__(256)
                       const int64_t* __restrict__ cell_cand, int64_t n_cells,
                       const uint32_t* __restrict__ win_cell, int64_t cb, int64_t ce,
                       uint32_t* __restrict__ qcount, unsigned long long* hits,
-                      unsigned long long* max_row) {
+                      unsigned long long* max_row, SymTables sym) {
   const int lane = lane_id();
   const int64_t pb = cell_start[cb], pe = cell_start[ce];
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -327,7 +400,7 @@ __global__ void __launch_bounds__(256)
     const int64_t p0 = w << 5, p = p0 + lane;
     const int64_t c = window_lane_cell(cell_start, n_cells, win_cell[w], p0);
     if (p < pb || p >= pe) continue;
-    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
+    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c], sym.fwd);
     unsigned cnt = 0;
     int b = 0;
     for (; b + 4 <= mr.nblk; b += 4) {
@@ -338,6 +411,9 @@ __global__ void __launch_bounds__(256)
       for (int u = 0; u < 4; ++u) cnt += __popc(row_bits(v[u], mr.shift));
     }
     for (; b < mr.nblk; ++b) cnt += __popc(row_bits(__ldg(mr.m + b), mr.shift));
+    if (sym.fwd)
+      cnt += backward_count(sym, masks, cell_mbase, cell_start, cell_cand, c,
+                            uint32_t(p - cell_start[c]));
     qcount[p] = cnt;
     tot += cnt;
     mx = max(mx, cnt);
@@ -409,7 +485,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
                      int64_t n_cells, const uint32_t* __restrict__ win_cell,
                      const uint32_t* __restrict__ qcount, const uint32_t* __restrict__ perm,
                      const int64_t* __restrict__ offsets, int64_t n, uint32_t* __restrict__ nbr,
-                     uint32_t* __restrict__ long_rows, unsigned long long* n_long, RowList rl) {
+                     uint32_t* __restrict__ long_rows, unsigned long long* n_long, RowList rl,
+                     SymTables sym) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   EmitSmem& sm = reinterpret_cast<EmitSmem*>(smem_raw)[warp];
@@ -447,7 +524,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = uint32_t(p);
     MaskRow mr{};
     if (pooled) {
-      mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c]);
+      mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c], sym.fwd);
       for (int b = 0; b < mr.nblk; b += 4) prefetch_l1(mr.m + b);
     }
     // run tables + block hints of the window's first kEmitCells cells
@@ -475,7 +552,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
     if (pooled) {
       uint32_t* col = pool + lane;
       const int ci = int(c - c0);
-      // 1. candidate offsets: 16 masks per batch, four blocks per packed word
+      // 1. candidate offsets (in the cell's list): 16 masks per batch, four blocks
+      //    per packed word
       int slot = 0;
       for (int b0 = 0; b0 < mr.nblk; b0 += 16) {
         unsigned long long mv[16];
@@ -489,18 +567,19 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
           while (wbits) {
             const int j = __ffs(wbits) - 1;
             wbits &= wbits - 1u;
-            col[slot * kPoolLd] = uint32_t(8 * (b0 + 4 * q + (j & 3)) + (j >> 2));
+            col[slot * kPoolLd] = mr.fwd + uint32_t(8 * (b0 + 4 * q + (j & 3)) + (j >> 2));
             ++slot;
           }
         }
       }
+      const int nf = slot;  // forward hits; the symmetric join's backward ones follow
       // 2. offsets -> positions: the block's run hint, then the (rare) steps to
       //    later runs when the block straddles a run boundary
-      if (ci < kEmitCells && mr.nblk <= kBlkTab) {
+      if (ci < kEmitCells && ((cell_cand[c] + 7) >> 3) <= kBlkTab) {
         const uint32_t* ro = sm.roff[ci];
         const uint32_t* rp = sm.rpos[ci];
         const unsigned char* br = sm.brun[ci];
-        for (int i = 0; i < len; ++i) {
+        for (int i = 0; i < nf; ++i) {
           const uint32_t t = col[i * kPoolLd];
           int r = br[t >> 3];
           while (ro[r + 1] <= t) ++r;
@@ -509,19 +588,23 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
       } else {  // many tiny cells in the window, or a very long list: global search
         const int64_t rb = cell_runs[c];
         const int nr = int(cell_runs[c + 1] - rb);
-        for (int i = 0; i < len; ++i)
+        for (int i = 0; i < nf; ++i)
           col[i * kPoolLd] = run_position(runs, run_off, rb, nr, col[i * kPoolLd]);
       }
       // 3. positions -> original ids, 16 gathers in flight
-      for (int i0 = 0; i0 < len; i0 += 16) {
+      for (int i0 = 0; i0 < nf; i0 += 16) {
         uint32_t v[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          v[u] = i0 + u < len ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
+          v[u] = i0 + u < nf ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          if (i0 + u < len) col[(i0 + u) * kPoolLd] = v[u];
+          if (i0 + u < nf) col[(i0 + u) * kPoolLd] = v[u];
       }
+      // 4. symmetric join: pairs with earlier neighbour cells, from their masks
+      if (sym.fwd)
+        emit_backward(sym, masks, cell_mbase, cell_start, cell_cand, perm, c,
+                      uint32_t(p - cell_start[c]), col, slot);
     }
     __syncwarp();
     pool_sort(pool, pooled ? len : 0);
@@ -566,9 +649,8 @@ __global__ void __launch_bounds__(256)
                      int64_t n_cells, const uint32_t* __restrict__ perm,
                      const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
                      const uint32_t* __restrict__ long_rows, const unsigned long long* n_long,
-                     uint32_t* __restrict__ big_rows, unsigned long long* n_big) {
+                     uint32_t* __restrict__ big_rows, unsigned long long* n_big, SymTables sym) {
   const int lane = lane_id();
-  const unsigned lt = lanemask_lt();
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const int64_t nl = int64_t(*n_long);
   for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32; i < nl; i += warps) {
@@ -583,7 +665,8 @@ __global__ void __launch_bounds__(256)
     const uint32_t id = perm[p];
     const int64_t dst = offsets[id];
     const int len = int(offsets[id + 1] - dst);
-    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, int64_t(p) - cell_start[c]);
+    const MaskRow mr = mask_row(masks, cell_mbase, cell_cand, c, int64_t(p) - cell_start[c],
+                                sym.fwd);
     uint32_t* row = nbr + dst;
     int base = 0;
     for (int b0 = 0; b0 < mr.nblk; b0 += 32) {
@@ -600,15 +683,27 @@ __global__ void __launch_bounds__(256)
       while (bits) {
         const int r = (__ffs(bits) - 1) >> 2;
         bits &= bits - 1u;
-        row[at++] = uint32_t(8 * b + r);
+        row[at++] = mr.fwd + uint32_t(8 * b + r);
       }
       base += __shfl_sync(0xffffffffu, incl, 31);
     }
-    (void)lt;
     __syncwarp();
     const int64_t rb = cell_runs[c];
     const int nr = int(cell_runs[c + 1] - rb);
-    for (int e = lane; e < len; e += 32) row[e] = perm[run_position(runs, run_off, rb, nr, row[e])];
+    for (int e = lane; e < base; e += 32) row[e] = perm[run_position(runs, run_off, rb, nr, row[e])];
+    // symmetric join: the pairs with earlier neighbour cells (rare long rows: one lane)
+    if (sym.fwd && lane == 0) {
+      int at = base;
+      for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c,
+                        uint32_t(int64_t(p) - cell_start[c]),
+                        [&](unsigned bits, int64_t qbase) {
+                          while (bits) {
+                            const int j = __ffs(bits) - 1;
+                            bits &= bits - 1u;
+                            row[at++] = perm[qbase + cand_bit_query(j)];
+                          }
+                        });
+    }
     __syncwarp();
     sort_long_row(row, len, id, big_rows, n_big);
   }
@@ -688,8 +783,118 @@ __global__ void huge_scatter_kernel(const int64_t* __restrict__ offsets, uint32_
   }
 }
 
+// ---------------------------------------------------------- symmetric join
+// Low-d symmetric join: the refine covers, for every cell B, only the suffix of
+// B's candidate list from B's own first point on (the cells >= B; fwd[B] is that
+// offset).  The pairs of B's queries with a neighbour cell X < B then sit in X's
+// masks, where B's points are candidates: the backward table lists, per cell B,
+// every such X with the offset of B's first point in X's refined suffix.
+// Position of pos in the list of cell c (runs are position-sorted): list offset.
+__device__ __forceinline__ uint32_t list_offset(const uint2* __restrict__ runs,
+                                                const uint32_t* __restrict__ run_off, int64_t rb,
+                                                int nr, uint32_t pos) {
+  int lo = 0, hi = nr;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (runs[rb + mid].x <= pos) lo = mid;
+    else hi = mid;
+  }
+  return run_off[rb + lo] + (pos - runs[rb + lo].x);
+}
+
+__global__ void sym_fwd_kernel(const int64_t* __restrict__ cell_start,
+                               const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
+                               const uint32_t* __restrict__ run_off, const uint32_t* __restrict__ pcell,
+                               int64_t n_cells, uint32_t* __restrict__ fwd,
+                               int64_t* __restrict__ bt_count) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rb = cell_runs[c];
+    const int nr = int(cell_runs[c + 1] - rb);
+    const uint32_t own = uint32_t(cell_start[c]);
+    fwd[c] = list_offset(runs, run_off, rb, nr, own);
+    int64_t cnt = 0;  // neighbour cells before c
+    for (int r = 0; r < nr; ++r) {
+      const uint2 run = runs[rb + r];
+      if (run.x >= own) break;
+      const int64_t first = pcell[run.x];
+      const int64_t last = run.y <= own ? int64_t(pcell[run.y - 1]) : c - 1;
+      cnt += last - first + 1;
+    }
+    bt_count[c] = cnt;
+  }
+}
+
+__global__ void sym_fill_kernel(const int64_t* __restrict__ cell_start,
+                                const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
+                                const uint32_t* __restrict__ run_off, const uint32_t* __restrict__ pcell,
+                                const uint32_t* __restrict__ fwd, int64_t n_cells,
+                                const int64_t* __restrict__ bt_start, uint2* __restrict__ bt) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rb = cell_runs[c];
+    const int nr = int(cell_runs[c + 1] - rb);
+    const uint32_t own = uint32_t(cell_start[c]);
+    int64_t out = bt_start[c];
+    for (int r = 0; r < nr; ++r) {
+      const uint2 run = runs[rb + r];
+      if (run.x >= own) break;
+      const int64_t first = pcell[run.x];
+      const int64_t last = run.y <= own ? int64_t(pcell[run.y - 1]) : c - 1;
+      for (int64_t x = first; x <= last; ++x) {
+        const int64_t xb = cell_runs[x];
+        const uint32_t off = list_offset(runs, run_off, xb, int(cell_runs[x + 1] - xb), own);
+        bt[out++] = make_uint2(uint32_t(x), off - fwd[x]);
+      }
+    }
+  }
+}
+
+// Warp per cell (lanes stride over its points: big cells stay parallel).
+__global__ void pcell_kernel(const int64_t* __restrict__ cell_start, int64_t n_cells,
+                             uint32_t* __restrict__ pcell) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps)
+    for (int64_t p = cell_start[c] + lane_id(); p < cell_start[c + 1]; p += 32) pcell[p] = uint32_t(c);
+}
+
+static SymTables sym_tables(const tj_ctx* ctx) {
+  if (!ctx->symmetric) return SymTables{nullptr, nullptr, nullptr};
+  return SymTables{ctx->fwd.as<uint32_t>(), ctx->bt_start.as<int64_t>(), ctx->bt.as<uint2>()};
+}
+
 static unsigned blocks_for(int64_t n, int threads) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), kNumSMs * 16)));
+}
+
+void build_symmetric_tables(tj_ctx* ctx, cudaStream_t s) {
+  const int64_t n = ctx->g.n, nc = ctx->g.n_cells;
+  ctx->pcell.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1), s);
+  pcell_kernel<<<blocks_for(nc * 32, 256), 256, 0, s>>>(ctx->cell_start.as<int64_t>(), nc,
+                                                        ctx->pcell.as<uint32_t>());
+  TJ_CHECK_LAUNCH();
+  ctx->fwd.ensure(sizeof(uint32_t) * std::max<int64_t>(nc, 1), s);
+  ctx->bt_start.ensure(sizeof(int64_t) * (nc + 1), s);
+  ctx->tmp64.ensure(sizeof(int64_t) * (nc + 1), s);
+  sym_fwd_kernel<<<blocks_for(nc, 128), 128, 0, s>>>(
+      ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+      ctx->run_off.as<uint32_t>(), ctx->pcell.as<uint32_t>(), nc, ctx->fwd.as<uint32_t>(),
+      ctx->tmp64.as<int64_t>());
+  TJ_CHECK_LAUNCH();
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(nc, 1), s);
+  scan_exclusive(LoadAt<int64_t>{ctx->tmp64.as<int64_t>()},
+                 StoreAt<int64_t>{ctx->bt_start.as<int64_t>()}, nc, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(ctx->bt_start.as<int64_t>() + nc, sc.total, sizeof(int64_t),
+                          cudaMemcpyDeviceToDevice, s));
+  // bound: every neighbour row of a cell holds <= 3 cells (13 backward cells at k = 4)
+  int rows = 1;
+  for (int j = 0; j < ctx->g.k - 1; ++j) rows *= 3;
+  ctx->bt.ensure(sizeof(uint2) * std::max<int64_t>(nc * int64_t(rows) * 3 / 2 + 1, 1), s);
+  sym_fill_kernel<<<blocks_for(nc, 128), 128, 0, s>>>(
+      ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
+      ctx->run_off.as<uint32_t>(), ctx->pcell.as<uint32_t>(), ctx->fwd.as<uint32_t>(), nc,
+      ctx->bt_start.as<int64_t>(), ctx->bt.as<uint2>());
+  TJ_CHECK_LAUNCH();
 }
 
 void build_window_cells(tj_ctx* ctx, cudaStream_t s) {
@@ -705,7 +910,8 @@ void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* 
   count_rows_kernel<<<kNumSMs * 8, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
-      ctx->win_cell.as<uint32_t>(), cb, ce, ctx->qcount.as<uint32_t>(), hits, max_row);
+      ctx->win_cell.as<uint32_t>(), cb, ce, ctx->qcount.as<uint32_t>(), hits, max_row,
+      sym_tables(ctx));
   TJ_CHECK_LAUNCH();
 }
 
@@ -834,14 +1040,15 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
         ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
         ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
-        offsets, n, nbr, long_rows, nbig + 2, rl);
+        offsets, n, nbr, long_rows, nbig + 2, rl, sym_tables(ctx));
     TJ_CHECK_LAUNCH();
   }
   long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
       ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
-      ctx->perm.as<uint32_t>(), offsets, nbr, long_rows, nbig + 2, fill, nbig);
+      ctx->perm.as<uint32_t>(), offsets, nbr, long_rows, nbig + 2, fill, nbig,
+      sym_tables(ctx));
   TJ_CHECK_LAUNCH();
   if (max_mask_row > kWarpSortMax)
     sort_big_rows(ctx, const_cast<int64_t*>(offsets), nbr, fill, nbig, s);
@@ -895,7 +1102,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
           ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
           ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc,
           ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
-          offsets, n, nbr, long_rows, nbig + 2, RowList{});
+          offsets, n, nbr, long_rows, nbig + 2, RowList{}, sym_tables(ctx));
       TJ_CHECK_LAUNCH();
       TJ_CUDA(cudaEventRecord(ctx->ev3, s));
       ctx->have_emit_timing = true;
@@ -904,7 +1111,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
         ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc, ctx->perm.as<uint32_t>(),
-        offsets, nbr, long_rows, nbig + 2, fill, nbig);
+        offsets, nbr, long_rows, nbig + 2, fill, nbig, sym_tables(ctx));
     TJ_CHECK_LAUNCH();
   } else {
     // pair path: rows in cell (position) order first, then sorted into place

@@ -615,9 +615,11 @@ struct MaskCountIn {
   const int64_t* cell_start;
   const int64_t* cand;
   int64_t cb;
+  const uint32_t* fwd;  // symmetric join: only blocks from the cell's own offset on
   __device__ int64_t operator()(int64_t i) const {
     const int64_t c = cb + i;
-    return ((cell_start[c + 1] - cell_start[c] + 7) / 8) * ((cand[c] + 7) / 8);
+    const int64_t nc = cand[c] - (fwd ? int64_t(fwd[c]) : 0);
+    return ((cell_start[c + 1] - cell_start[c] + 7) / 8) * ((nc + 7) / 8);
   }
 };
 
@@ -627,7 +629,8 @@ void build_mask_bases(tj_ctx* ctx, int64_t cb, int64_t ce, cudaStream_t s) {
   if (n <= 0) return;
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
   ctx->cell_mbase.ensure(sizeof(int64_t) * (n + 1), s);
-  scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb},
+  scan_exclusive(MaskCountIn{ctx->cell_start.as<int64_t>(), ctx->cell_cand.as<int64_t>(), cb,
+                             ctx->symmetric ? ctx->fwd.as<uint32_t>() : nullptr},
                  StoreAt<int64_t>{ctx->cell_mbase.as<int64_t>()}, n, sc, s);
 }
 

@@ -92,6 +92,8 @@ struct RefineArgs {
   unsigned long long* masks;     // low-d hit masks
   const int64_t* cell_mbase;     // first mask of cell c at cell_mbase[c - cell_base]
   int64_t cell_base;
+  const uint32_t* fwd;           // low-d symmetric join: first candidate offset refined per cell
+                                 // (the cell's own position in its list); nullptr = 0
   int d, d_pad, nchunks;
   double eps_sq;
   double guard_rel;        // guard band = guard_rel * (qn + max_norm)
@@ -125,6 +127,9 @@ struct tj_ctx {
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;
   // results
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
+  // low-d symmetric join: per-cell forward offset, backward-cell table (CSR by cell)
+  tj::DevBuf fwd, bt_start, bt;
+  bool symmetric = true;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
   tj::DevBuf ipos, pcell;        // id-range position lists (2 x n: sort ping-pong), position -> cell
   tj::DevBuf chunk_key;          // sort keys of the position lists
@@ -187,6 +192,7 @@ void permute_columns(const double* src, int64_t n, int d, int64_t ld, const int*
 void brute_force_join(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld, double eps,
                       int64_t* offsets, uint32_t* nbr, int64_t* total, cudaStream_t s);
 void build_window_cells(tj_ctx* ctx, cudaStream_t s);
+void build_symmetric_tables(tj_ctx* ctx, cudaStream_t s);
 // shard.cu (multi-GPU strong layout)
 void shard_bounds(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int pdims, double eps,
                   int64_t* lo, int64_t* hi, cudaStream_t s);

@@ -173,10 +173,13 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
 // candidates at a time and every 8-candidate block is multiplied against the
 // NG query fragments back to back (independent DMMAs in flight), then
 // compared and balloted.
+// Blocks cover the item's candidates [s0, total) of the cell's list (s0 = 0, or the
+// cell's own offset in the symmetric join).
 template <bool FOLD, int NG, int R, bool U2ALL>
 __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& it, LowStage* ring,
                                           uint32_t* wbuf, unsigned long long* mrow, int nblk,
-                                          uint32_t total, uint32_t r_off, uint32_t r_pos, int nr) {
+                                          uint32_t s0, uint32_t total, uint32_t r_off,
+                                          uint32_t r_pos, int nr) {
   const int lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
   const int nq = int(it.nq);
@@ -202,9 +205,10 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
     }
   }
   const int nst = (nblk + 7) >> 3;
-  int rc = 0;  // run containing the first candidate of the next stage to issue
+  // run containing the first candidate of the next stage to issue
+  int rc = __popc(__ballot_sync(0xffffffffu, lane < nr && r_off <= s0)) - 1;
   auto issue = [&](int st, LowStage* s) {
-    const uint32_t base = uint32_t(st) * kStageCands;
+    const uint32_t base = s0 + uint32_t(st) * kStageCands;
     const uint32_t t0 = base + lane, t1 = t0 + 32;
     uint32_t p0 = 0, p1 = 0;
     int r = rc;
@@ -303,29 +307,33 @@ __global__ void __launch_bounds__(kLowThreads, MINB) refine_lowd_kernel(RefineAr
     // (<= 27 runs for k <= 4); lanes past the last run hold the list length
     const int64_t rb = a.cell_runs[it.cell], re = a.cell_runs[it.cell + 1];
     const int nr = int(re - rb);
-    const uint32_t total = it.s1;  // low-d items cover the whole list (s0 == 0)
+    const uint32_t total = it.s1;  // low-d items reach the end of the list
+    // symmetric join: only candidates from the cell itself on (cells >= it.cell);
+    // the pairs with earlier cells come from those cells' masks (finalize.cu)
+    const uint32_t s0 = a.fwd ? a.fwd[it.cell] : 0u;
     uint32_t r_off = total, r_pos = 0;
     if (lane < nr) {
       r_off = a.run_off[rb + lane];
       r_pos = a.runs[rb + lane].x;
     }
-    const int nblk = int((total + 7) >> 3);
-    st_tiles += uint64_t(ng) * uint64_t(nblk);
+    const int nblk = int((total - s0 + 7) >> 3);
+    // JoinStats in the reference's tiling of the whole list (join.py:257-261, 273)
+    st_tiles += uint64_t(ng) * uint64_t((total + 7) >> 3);
     st_refined += uint64_t(it.nq) * total;
     // this item's masks: (group, block) order, group (q0 - cell start) / 8 of the cell
     const int64_t cs = a.cell_start[it.cell];
     unsigned long long* mrow = a.masks + a.cell_mbase[it.cell - a.cell_base] +
                                ((int64_t(it.q0) - cs) >> 3) * nblk;
     switch (ng) {
-      case 1: lowd_item<FOLD, 1, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
-      case 2: lowd_item<FOLD, 2, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr); break;
+      case 1: lowd_item<FOLD, 1, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, s0, total, r_off, r_pos, nr); break;
+      case 2: lowd_item<FOLD, 2, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, s0, total, r_off, r_pos, nr); break;
       case 3:
         if constexpr (NGMAX >= 3)
-          lowd_item<FOLD, 3, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
+          lowd_item<FOLD, 3, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, s0, total, r_off, r_pos, nr);
         break;
       default:
         if constexpr (NGMAX >= 4)
-          lowd_item<FOLD, 4, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, total, r_off, r_pos, nr);
+          lowd_item<FOLD, 4, R, U2ALL>(a, it, ring, wbuf, mrow, nblk, s0, total, r_off, r_pos, nr);
         break;
     }
   }

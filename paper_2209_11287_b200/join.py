@@ -19,6 +19,7 @@ value lies inside its rounding guard band with the direct form.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -376,6 +377,10 @@ class DeviceJoin:
         if cell_range is not None:
             lo, hi = cell_range
             batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
+        # the low-d symmetric join (TJ_SYMMETRIC=0 turns it off) needs every earlier
+        # cell in the same result set: not for a cell range starting past cell 0
+        self.ctx.set_symmetric(os.environ.get("TJ_SYMMETRIC", "1") != "0"
+                               and (cell_range is None or cell_range[0] == 0))
         appends = self.appends_pairs()
         if appends and batches:
             est = self.estimate_pairs(batches)
