@@ -116,6 +116,13 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
  * cell range that does not start at cell 0 (the multi-GPU shards) turn it off.
  * Takes effect at the next tj_refine. */
 int tj_set_symmetric(tj_ctx* ctx, int32_t on);
+/* Symmetric low-d join over a cell range past cell 0 (a multi-GPU shard): refine
+ * the earlier cells [cell_begin, cell_end) for their hit masks only -- their rows,
+ * counts and stats are not part of the result set; the rows of the cells refined
+ * next read their pairs with these cells from the masks.  No-op for other kernels
+ * or with the symmetric join off.  Asynchronous. */
+int tj_refine_masks(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+                    int64_t cell_end, void* stream);
 /* Result pairs since the last tj_reset_results (synchronous).  The count is exact
  * even past the append buffer's capacity (CUDA-core and high-d DMMA kernels
  * append pairs; the low-d DMMA kernel records hit masks and never overflows);

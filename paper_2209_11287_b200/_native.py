@@ -55,6 +55,7 @@ SIGNATURES = {
     "tj_reserve_results": (_i32, [_vp, _i64]),
     "tj_checkpoint_results": (_i32, [_vp, _vp]),
     "tj_set_symmetric": (_i32, [_vp, _i32]),
+    "tj_refine_masks": (_i32, [_vp, _i32, _i32, _i64, _i64, _vp]),
     "tj_estimate_pairs": (_i32, [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64,
                                  ctypes.POINTER(_f64), _vp]),
     "tj_rollback_results": (_i32, [_vp, _i64, _i64, _vp]),
@@ -210,6 +211,12 @@ class Context:
                                                int(cell_end), int(samples), int(seed),
                                                ctypes.byref(rate), s.cuda_stream))
         return float(rate.value)
+
+    def refine_masks(self, kernel: int, short_circuit: bool, cell_begin: int, cell_end: int,
+                     stream=None):
+        s = stream or self.stream()
+        self._check(self.lib.tj_refine_masks(self.handle, kernel, int(bool(short_circuit)),
+                                             cell_begin, cell_end, s.cuda_stream))
 
     def set_symmetric(self, on: bool):
         self._check(self.lib.tj_set_symmetric(self.handle, int(bool(on))))

@@ -381,12 +381,40 @@ static void launch_refine(const tj_ctx* ctx, const RefinePlan& rp, const RefineA
   else launch_refine_core(a, rp.variant, s);
 }
 
-int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
-              int64_t cell_end, void* stream) {
+static void refine_range(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+                         int64_t cell_end, cudaStream_t s, bool count_rows);
+
+int tj_refine_masks(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+                    int64_t cell_end, void* stream) {
   if (!ctx) return TJ_EINVAL;
   return guarded(ctx, [&] {
     require_grid(ctx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const RefinePlan rp = plan_refine(ctx, kernel);
+    if (!rp.lowd || !ctx->symmetric) return;  // only the symmetric low-d join reads them
+    // the counters (stats, totals) stay as they were: these cells are not this
+    // result set's rows, only the masks its rows read back
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx) + 1, counters(ctx), sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+    refine_range(ctx, kernel, short_circuit, cell_begin, cell_end, s, false);
+    TJ_CUDA(cudaMemcpyAsync(counters(ctx), counters(ctx) + 1, sizeof(DevCounters),
+                            cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+              int64_t cell_end, void* stream) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    refine_range(ctx, kernel, short_circuit, cell_begin, cell_end,
+                 static_cast<cudaStream_t>(stream), true);
+  });
+}
+
+static void refine_range(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
+                         int64_t cell_end, cudaStream_t s, bool count_rows) {
+  {
+    require_grid(ctx);
     ctx->last_stream = s;
     const GridState& g = ctx->g;
     if (kernel < TJ_KERNEL_CORE || kernel > TJ_KERNEL_CORE_EXPANDED)
@@ -411,9 +439,9 @@ int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_b
     TJ_CUDA(cudaEventRecord(ctx->ev1, s));
     ctx->have_refine_timing = true;
     // low-d rows are counted from the hit masks (pairs per query + total hits)
-    if (rp.lowd)
+    if (rp.lowd && count_rows)
       launch_count_rows(ctx, cell_begin, cell_end, &counters(ctx)->hits, &counters(ctx)->max_row, s);
-  });
+  }
 }
 
 __global__ void zero_sample_counts_kernel(const WorkItem* __restrict__ items, int64_t n_items,

@@ -377,16 +377,19 @@ class DeviceJoin:
         if cell_range is not None:
             lo, hi = cell_range
             batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
-        # the low-d symmetric join (TJ_SYMMETRIC=0 turns it off) needs every earlier
-        # cell in the same result set: not for a cell range starting past cell 0
-        self.ctx.set_symmetric(os.environ.get("TJ_SYMMETRIC", "1") != "0"
-                               and (cell_range is None or cell_range[0] == 0))
+        # the low-d symmetric join (TJ_SYMMETRIC=0 turns it off) reads every earlier
+        # cell's masks: for a cell range past cell 0 (a multi-GPU shard) the earlier
+        # cells -- the shard's halo -- are refined for their masks only, below
+        symmetric = os.environ.get("TJ_SYMMETRIC", "1") != "0"
+        self.ctx.set_symmetric(symmetric)
         appends = self.appends_pairs()
         if appends and batches:
             est = self.estimate_pairs(batches)
         self.ctx.reset_results()
         if appends and batches:
             self.ctx.reserve_results(est)
+        if symmetric and batches and batches[0][0] > 0:
+            self.ctx.refine_masks(self.kernel, cfg.short_circuit, 0, batches[0][0])
         total = 0
         for batch_no, (start, stop) in enumerate(batches):
             if appends:
