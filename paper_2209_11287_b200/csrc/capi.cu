@@ -64,6 +64,7 @@ static void ensure_masks(tj_ctx* ctx, cudaStream_t s) {
   if (ctx->masks_ready) return;
   if (ctx->symmetric) build_symmetric_tables(ctx, s);
   build_mask_bases(ctx, 0, ctx->g.n_cells, s);
+  if (ctx->symmetric) build_bt_desc(ctx, s);
   ctx->masks.ensure(sizeof(unsigned long long) * std::max<int64_t>(ctx->g.tiles, 1), s);
   build_window_cells(ctx, s);
   ctx->masks_ready = true;
@@ -144,7 +145,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
                     &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
                     &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell,
-                    &ctx->fwd,      &ctx->bt_start,  &ctx->bt,       &ctx->chunk_key};
+                    &ctx->fwd,      &ctx->bt_start,  &ctx->bt,       &ctx->chunk_key,
+                    &ctx->bt_desc};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);

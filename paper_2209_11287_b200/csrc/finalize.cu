@@ -288,10 +288,21 @@ __device__ __forceinline__ int64_t window_lane_cell(const int64_t* __restrict__ 
 }
 
 // Symmetric join tables (build_symmetric_tables); fwd == nullptr: plain join.
+// One backward entry of cell c: an earlier neighbour cell X, with what a row of c
+// needs to read X's masks (built once per grid after the mask layout).
+struct alignas(16) BtDesc {
+  long long mbase;   // X's first mask
+  unsigned nblk;     // X's refined blocks per query group
+  unsigned rel;      // offset of c's first point in X's refined suffix
+  unsigned qbase;    // X's first position
+  unsigned ng;       // X's query groups
+  unsigned pad[2];
+};
+
 struct SymTables {
   const uint32_t* fwd;       // per cell: list offset of the cell's own first point
   const int64_t* bt_start;   // per cell: backward entries [bt_start[c], bt_start[c+1])
-  const uint2* bt;           // (cell X < c, offset of c's first point in X's refined suffix)
+  const BtDesc* desc;        // the entries
 };
 
 struct MaskRow {
@@ -323,24 +334,42 @@ __device__ __forceinline__ unsigned cand_row_bits(unsigned long long m, int r) {
 // Backward part of a row (symmetric join): the point at offset `rel` of cell c
 // is a candidate of every earlier neighbour cell X; its pairs with X's queries
 // are candidate row (off & 7) of block (off >> 3) in each of X's query groups.
+// Entries go four at a time: their descriptors, then their masks, are loaded
+// before any is used (the loads are independent; only their latency matters).
 template <class F>
 __device__ __forceinline__ void for_backward_hits(const SymTables& sym,
                                                   const unsigned long long* __restrict__ masks,
-                                                  const int64_t* __restrict__ cell_mbase,
-                                                  const int64_t* __restrict__ cell_start,
-                                                  const int64_t* __restrict__ cell_cand,
                                                   int64_t c, uint32_t rel, F&& f) {
   const int64_t e1 = sym.bt_start[c + 1];
-  for (int64_t e = sym.bt_start[c]; e < e1; ++e) {
-    const uint2 xo = sym.bt[e];
-    const int64_t x = xo.x;
-    const uint32_t off = xo.y + rel;
-    const int64_t xs = cell_start[x];
-    const int ngx = int((cell_start[x + 1] - xs + 7) >> 3);
-    const int nblkx = int((cell_cand[x] - sym.fwd[x] + 7) >> 3);
-    const unsigned long long* m = masks + cell_mbase[x] + (off >> 3);
-    const int r = int(off & 7);
-    for (int g = 0; g < ngx; ++g) f(cand_row_bits(__ldg(m + int64_t(g) * nblkx), r), xs + 8 * g);
+  for (int64_t e0 = sym.bt_start[c]; e0 < e1; e0 += 4) {
+    BtDesc dd[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (e0 + u < e1) {
+        dd[u] = sym.desc[e0 + u];
+      } else {
+        dd[u].ng = 0;
+        dd[u].mbase = 0;
+        dd[u].nblk = dd[u].rel = dd[u].qbase = 0;
+      }
+    }
+    unsigned long long mv[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long* m = masks + dd[u].mbase + ((dd[u].rel + rel) >> 3);
+      mv[u][0] = dd[u].ng > 0 ? __ldg(m) : 0ull;
+      mv[u][1] = dd[u].ng > 1 ? __ldg(m + dd[u].nblk) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = int((dd[u].rel + rel) & 7);
+      if (dd[u].ng > 0) f(cand_row_bits(mv[u][0], r), dd[u].qbase);
+      if (dd[u].ng > 1) f(cand_row_bits(mv[u][1], r), dd[u].qbase + 8);
+      for (unsigned g = 2; g < dd[u].ng; ++g) {  // cells of > 16 points: rare at low d
+        const unsigned long long* m = masks + dd[u].mbase + ((dd[u].rel + rel) >> 3);
+        f(cand_row_bits(__ldg(m + int64_t(g) * dd[u].nblk), r), dd[u].qbase + 8 * g);
+      }
+    }
   }
 }
 
@@ -350,32 +379,51 @@ __device__ __forceinline__ int backward_count(const SymTables& sym,
                                               const int64_t* __restrict__ cell_start,
                                               const int64_t* __restrict__ cell_cand, int64_t c,
                                               uint32_t rel) {
+  (void)cell_mbase;
+  (void)cell_start;
+  (void)cell_cand;
   int cnt = 0;
-  for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c, rel,
-                    [&](unsigned bits, int64_t) { cnt += __popc(bits); });
+  for_backward_hits(sym, masks, c, rel, [&](unsigned bits, unsigned) { cnt += __popc(bits); });
   return cnt;
 }
 
 // Query column of bit j of cand_row_bits: bits 0..3 -> 0, 2, 4, 6; 4..7 -> 1, 3, 5, 7.
 __device__ __forceinline__ int cand_bit_query(int j) { return j < 4 ? 2 * j : 2 * (j - 4) + 1; }
 
-// Original ids of a row's backward hits into its pool column from `slot` on.
+// Positions of a row's backward hits into its pool column from `slot` on.
 __device__ __noinline__ void emit_backward(const SymTables& sym,
                                            const unsigned long long* __restrict__ masks,
-                                           const int64_t* __restrict__ cell_mbase,
-                                           const int64_t* __restrict__ cell_start,
-                                           const int64_t* __restrict__ cell_cand,
-                                           const uint32_t* __restrict__ perm, int64_t c,
-                                           uint32_t rel, uint32_t* col, int slot) {
-  for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c, rel,
-                    [&](unsigned bits, int64_t qbase) {
-                      while (bits) {
-                        const int j = __ffs(bits) - 1;
-                        bits &= bits - 1u;
-                        col[slot * kPoolLd] = __ldg(perm + qbase + cand_bit_query(j));
-                        ++slot;
-                      }
-                    });
+                                           int64_t c, uint32_t rel, uint32_t* col, int slot) {
+  for_backward_hits(sym, masks, c, rel, [&](unsigned bits, unsigned qbase) {
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      col[slot * kPoolLd] = qbase + unsigned(cand_bit_query(j));
+      ++slot;
+    }
+  });
+}
+
+// desc[e] for every backward entry (after the mask layout is known).
+__global__ void bt_desc_kernel(const uint2* __restrict__ bt, const int64_t* __restrict__ n_entries_dev,
+                               const int64_t* __restrict__ cell_start,
+                               const int64_t* __restrict__ cell_cand,
+                               const int64_t* __restrict__ cell_mbase,
+                               const uint32_t* __restrict__ fwd, BtDesc* __restrict__ desc) {
+  const int64_t n_entries = *n_entries_dev;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n_entries;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const uint2 xo = bt[e];
+    const int64_t x = xo.x;
+    BtDesc d;
+    d.mbase = cell_mbase[x];
+    d.nblk = unsigned((cell_cand[x] - fwd[x] + 7) >> 3);
+    d.rel = xo.y;
+    d.qbase = unsigned(cell_start[x]);
+    d.ng = unsigned((cell_start[x + 1] - cell_start[x] + 7) >> 3);
+    d.pad[0] = d.pad[1] = 0;
+    desc[e] = d;
+  }
 }
 
 __device__ __forceinline__ unsigned row_bits(unsigned long long m, int shift) {
@@ -591,20 +639,19 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
         for (int i = 0; i < nf; ++i)
           col[i * kPoolLd] = run_position(runs, run_off, rb, nr, col[i * kPoolLd]);
       }
-      // 3. positions -> original ids, 16 gathers in flight
-      for (int i0 = 0; i0 < nf; i0 += 16) {
+      // 3. symmetric join: positions of the pairs with earlier neighbour cells,
+      //    from their masks
+      if (sym.fwd) emit_backward(sym, masks, c, uint32_t(p - cell_start[c]), col, nf);
+      // 4. positions -> original ids, 16 gathers in flight
+      for (int i0 = 0; i0 < len; i0 += 16) {
         uint32_t v[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          v[u] = i0 + u < nf ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
+          v[u] = i0 + u < len ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          if (i0 + u < nf) col[(i0 + u) * kPoolLd] = v[u];
+          if (i0 + u < len) col[(i0 + u) * kPoolLd] = v[u];
       }
-      // 4. symmetric join: pairs with earlier neighbour cells, from their masks
-      if (sym.fwd)
-        emit_backward(sym, masks, cell_mbase, cell_start, cell_cand, perm, c,
-                      uint32_t(p - cell_start[c]), col, slot);
     }
     __syncwarp();
     pool_sort(pool, pooled ? len : 0);
@@ -694,9 +741,8 @@ __global__ void __launch_bounds__(256)
     // symmetric join: the pairs with earlier neighbour cells (rare long rows: one lane)
     if (sym.fwd && lane == 0) {
       int at = base;
-      for_backward_hits(sym, masks, cell_mbase, cell_start, cell_cand, c,
-                        uint32_t(int64_t(p) - cell_start[c]),
-                        [&](unsigned bits, int64_t qbase) {
+      for_backward_hits(sym, masks, c, uint32_t(int64_t(p) - cell_start[c]),
+                        [&](unsigned bits, unsigned qbase) {
                           while (bits) {
                             const int j = __ffs(bits) - 1;
                             bits &= bits - 1u;
@@ -860,7 +906,8 @@ __global__ void pcell_kernel(const int64_t* __restrict__ cell_start, int64_t n_c
 
 static SymTables sym_tables(const tj_ctx* ctx) {
   if (!ctx->symmetric) return SymTables{nullptr, nullptr, nullptr};
-  return SymTables{ctx->fwd.as<uint32_t>(), ctx->bt_start.as<int64_t>(), ctx->bt.as<uint2>()};
+  return SymTables{ctx->fwd.as<uint32_t>(), ctx->bt_start.as<int64_t>(),
+                   ctx->bt_desc.as<BtDesc>()};
 }
 
 static unsigned blocks_for(int64_t n, int threads) {
@@ -894,6 +941,19 @@ void build_symmetric_tables(tj_ctx* ctx, cudaStream_t s) {
       ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
       ctx->run_off.as<uint32_t>(), ctx->pcell.as<uint32_t>(), ctx->fwd.as<uint32_t>(), nc,
       ctx->bt_start.as<int64_t>(), ctx->bt.as<uint2>());
+  TJ_CHECK_LAUNCH();
+}
+
+void build_bt_desc(tj_ctx* ctx, cudaStream_t s) {
+  const int64_t nc = ctx->g.n_cells;
+  int rows = 1;
+  for (int j = 0; j < ctx->g.k - 1; ++j) rows *= 3;
+  const int64_t bound = std::max<int64_t>(nc * int64_t(rows) * 3 / 2 + 1, 1);
+  ctx->bt_desc.ensure(sizeof(BtDesc) * bound, s);
+  bt_desc_kernel<<<blocks_for(bound, 256), 256, 0, s>>>(
+      ctx->bt.as<uint2>(), ctx->bt_start.as<int64_t>() + nc, ctx->cell_start.as<int64_t>(),
+      ctx->cell_cand.as<int64_t>(), ctx->cell_mbase.as<int64_t>(), ctx->fwd.as<uint32_t>(),
+      ctx->bt_desc.as<BtDesc>());
   TJ_CHECK_LAUNCH();
 }
 

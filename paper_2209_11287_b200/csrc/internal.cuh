@@ -128,7 +128,7 @@ struct tj_ctx {
   // results
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
   // low-d symmetric join: per-cell forward offset, backward-cell table (CSR by cell)
-  tj::DevBuf fwd, bt_start, bt;
+  tj::DevBuf fwd, bt_start, bt, bt_desc;
   bool symmetric = true;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
   tj::DevBuf ipos, pcell;        // id-range position lists (2 x n: sort ping-pong), position -> cell
@@ -193,6 +193,7 @@ void brute_force_join(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld
                       int64_t* offsets, uint32_t* nbr, int64_t* total, cudaStream_t s);
 void build_window_cells(tj_ctx* ctx, cudaStream_t s);
 void build_symmetric_tables(tj_ctx* ctx, cudaStream_t s);
+void build_bt_desc(tj_ctx* ctx, cudaStream_t s);
 // shard.cu (multi-GPU strong layout)
 void shard_bounds(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int pdims, double eps,
                   int64_t* lo, int64_t* hi, cudaStream_t s);
