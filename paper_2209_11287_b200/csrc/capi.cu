@@ -312,7 +312,7 @@ int tj_rollback_results(tj_ctx* ctx, int64_t cell_begin, int64_t cell_end, void*
 
 // Which refine kernel a tj_refine call runs and how it cuts work items.
 struct RefinePlan {
-  bool lowd, dmma, gram;
+  bool lowd, dmma, gram, core_gram;
   int variant;     // CUDA-core variant (refine_core.cu)
   int qpi;         // queries per work item
   int64_t target;  // candidate-slice target of build_work_items
@@ -327,17 +327,20 @@ static RefinePlan plan_refine(const tj_ctx* ctx, int32_t kernel) {
   r.lowd = r.dmma && g.d_pad == 4;
   // big cells at d_pad >= 12: the CTA-blocked Gram kernel (refine_gram.cu)
   r.gram = r.dmma && !r.lowd && gram_applies(g.d_pad, g.n, g.n_cells);
+  // the expanded form in DFMA on big cells: the same CTA blocking on CUDA cores
+  r.core_gram = kernel == TJ_KERNEL_CORE_EXPANDED && norms_ok && g.d <= 64 &&
+                gram_applies(g.d_pad, g.n, g.n_cells);
   r.variant = kernel == TJ_KERNEL_CORE_FMA                   ? 1
               : kernel == TJ_KERNEL_CORE_EXPANDED && norms_ok ? 2
                                                               : 0;
-  r.qpi = r.lowd   ? lowd_queries_per_item(g.n, g.n_cells)
-          : r.gram ? kGramQueries
+  r.qpi = r.lowd                  ? lowd_queries_per_item(g.n, g.n_cells)
+          : (r.gram || r.core_gram) ? kGramQueries
           : r.dmma ? tc_queries_per_item(g.d_pad, g.n, g.n_cells)
                    : core_queries_per_item(g.d, g.d_pad);
   // lowd: items never split a candidate list (each query row comes from one item);
   // gram: 64-query items x 32k-candidate slices
-  r.target = r.lowd   ? (int64_t(1) << 60)
-             : r.gram ? int64_t(kGramQueries) * kGramSlice
+  r.target = r.lowd                  ? (int64_t(1) << 60)
+             : (r.gram || r.core_gram) ? int64_t(kGramQueries) * kGramSlice
                       : std::max<int64_t>(g.candidates / (int64_t(kNumSMs) * 8), 1 << 16);
   return r;
 }
@@ -378,7 +381,8 @@ static void launch_refine(const tj_ctx* ctx, const RefinePlan& rp, const RefineA
                           cudaStream_t s) {
   const GridState& g = ctx->g;
   if (rp.lowd) launch_refine_lowd(a, g.n, g.n_cells, s);
-  else if (rp.gram) launch_refine_gram(a, s);
+  else if (rp.gram) launch_refine_gram(a, false, s);
+  else if (rp.core_gram) launch_refine_gram(a, true, s);
   else if (rp.dmma) launch_refine_tc(a, g.n, g.n_cells, s);
   else launch_refine_core(a, rp.variant, s);
 }

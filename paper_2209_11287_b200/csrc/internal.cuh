@@ -174,7 +174,7 @@ int lowd_queries_per_item(int64_t n, int64_t n_cells);
 constexpr int kGramQueries = 64;
 constexpr int64_t kGramSlice = 32768;
 bool gram_applies(int d_pad, int64_t n, int64_t n_cells);
-void launch_refine_gram(const RefineArgs& a, cudaStream_t s);
+void launch_refine_gram(const RefineArgs& a, bool cuda_cores, cudaStream_t s);
 int core_queries_per_item(int d, int d_pad);
 int tc_queries_per_item(int d_pad, int64_t n, int64_t n_cells);
 // finalize.cu

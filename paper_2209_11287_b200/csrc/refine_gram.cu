@@ -34,16 +34,22 @@ constexpr int kGramQ = 64;   // queries per item
 constexpr int kGramC = 64;   // candidates per stage
 constexpr int kGramStages = 2;
 
-template <int NCH>
+// CORE = false: DMMA fragments.  CORE = true: the same blocking on CUDA cores --
+// the expanded form in DFMA, each thread a 4-query x 8-candidate register block
+// (kernel="core_expanded" on big cells: the tensor-core comparison with identical
+// algebra, staging and epilogue).
+template <int NCH, bool CORE = false>
 struct GramShape {
   static constexpr int DP = 4 * NCH;
-  static constexpr int STRIDE = (DP % 8 == 0) ? DP + 4 : DP;  // conflict-free fragment rows
+  // DMMA: conflict-free fragment rows; CORE: rows 8 apart (a thread's candidates)
+  // and 16 apart (its queries) hit distinct banks with 16-byte loads
+  static constexpr int STRIDE = CORE ? DP + 2 : ((DP % 8 == 0) ? DP + 4 : DP);
   static constexpr int PPR = DP / 2;                           // 16-byte pieces per row
 };
 
-template <int NCH>
+template <int NCH, bool CORE = false>
 struct GramSmem {
-  using S = GramShape<NCH>;
+  using S = GramShape<NCH, CORE>;
   double q[kGramQ][S::STRIDE];                   // -2 * query coordinates
   double c[kGramStages][kGramC][S::STRIDE];      // candidate coordinates
   double cn[kGramStages][kGramC];                // |c|^2 (padding rows: kPadNorm)
@@ -84,13 +90,80 @@ __device__ __noinline__ uint2 gram_recheck(const double* P, int dp, int d, doubl
   return make_uint2(__ballot_sync(0xffffffffu, p0), __ballot_sync(0xffffffffu, p1));
 }
 
-template <int NCH, int MINB>
+// One 64 x 64 stage on CUDA cores: thread (qg, cg) = (threadIdx.x >> 3, & 7) owns
+// queries qg + 16k (k < 4) x candidates cg + 8i (i < 8); two dims per 16-byte load,
+// 64 DFMA per 12 loads; acc starts at |c|^2 and adds (-2q).c (the expanded form).
+template <class S, class Q, class C>
+__device__ __forceinline__ void gram_core_stage(const RefineArgs& a, const Q& sq, const C& sc,
+                                                const double* cn, const double* thr_s,
+                                                const double* tlo_s, const uint32_t* pos,
+                                                uint32_t q0, HitBuffer& hb, uint2* hits,
+                                                unsigned (&qc)[4][2],
+                                                unsigned long long& rechecks) {
+  const int qg = threadIdx.x >> 3, cg = threadIdx.x & 7;
+  const unsigned lt = lanemask_lt();
+  double acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double c0 = cn[cg + 8 * i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k][i] = c0;
+  }
+#pragma unroll 2
+  for (int j = 0; j < S::DP; j += 2) {
+    double2 qv[4], cv[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qv[k] = *reinterpret_cast<const double2*>(&sq[qg + 16 * k][j]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cv[i] = *reinterpret_cast<const double2*>(&sc[cg + 8 * i][j]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[k][i] = __fma_rn(qv[k].x, cv[i].x, acc[k][i]);
+        acc[k][i] = __fma_rn(qv[k].y, cv[i].y, acc[k][i]);
+      }
+  }
+  double thr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) thr[k] = thr_s[qg + 16 * k];
+  bool pk[4] = {false, false, false, false};
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pk[k] = pk[k] || (acc[k][i] <= thr[k]);
+  if (!__any_sync(0xffffffffu, (pk[0] || pk[1]) || (pk[2] || pk[3]))) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double tlo = tlo_s[qg + 16 * k];
+    const uint32_t qpos = q0 + qg + 16 * k;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bool p = acc[k][i] <= thr[k];
+      if (!__any_sync(0xffffffffu, p)) continue;
+      const uint32_t cpos = pos[cg + 8 * i];
+      const bool band = p && acc[k][i] > tlo;
+      if (band) {  // inside the guard band: the reference direct form decides
+        ++rechecks;
+        p = direct_form_le(a.P, S::DP, a.d, qpos, cpos, a.eps_sq);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, p);
+      if (!m) continue;
+      hb.reserve(__popc(m), hits, a);
+      if (p) hits[hb.count + __popc(m & lt)] = make_uint2(qpos, cpos);
+      hb.count += __popc(m);
+      qc[k][0] += p;
+    }
+  }
+}
+
+template <int NCH, int MINB, bool CORE>
 __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineArgs a) {
-  using S = GramShape<NCH>;
+  using S = GramShape<NCH, CORE>;
   constexpr int DP = S::DP, PPR = S::PPR;
   constexpr int kUnroll = NCH >= 8 ? 4 : 2;  // chunks whose fragment loads are hoisted together
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GramSmem<NCH>& sm = *reinterpret_cast<GramSmem<NCH>*>(smem_raw);
+  GramSmem<NCH, CORE>& sm = *reinterpret_cast<GramSmem<NCH, CORE>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int row = lane >> 2, col = lane & 3;
   const unsigned lt = lanemask_lt();
@@ -98,7 +171,7 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
   uint2* hits = sm.hits[warp];
   HitBuffer hb;
   const double eps_sq = a.eps_sq;
-  unsigned long long st_tiles_ref = 0;
+  unsigned long long st_tiles_ref = 0, rechecks = 0;
   __shared__ unsigned long long s_item;
 
   for (;;) {
@@ -131,7 +204,7 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
       sm.thr[q] = v ? eps_sq - qn + guard : -INFINITY;
       sm.tlo[q] = v ? eps_sq - qn - guard : INFINITY;
     }
-    unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    unsigned qc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // CORE: qc[k][0], query qg + 16k
     if (threadIdx.x == 0) st_tiles_ref += uint64_t((nq + 7) >> 3) * ((s1 - s0 + 7) >> 3);
 
     // stage st: candidates s0 + 64 st + r.  Thread r < 64 follows offsets
@@ -197,6 +270,10 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
       gram_wait<1>();
       __syncthreads();
       const int buf = st % kGramStages;
+      if constexpr (CORE) {
+        gram_core_stage<S>(a, sm.q, sm.c[buf], sm.cn[buf], sm.thr, sm.tlo, sm.pos[st % 3], it.q0,
+                           hb, hits, qc, rechecks);
+      } else {
       double acc[4][4][2];  // [candidate block][query group][value]
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -265,9 +342,23 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
           }
         }
       }
+      }  // DMMA path
     }
     gram_wait<0>();
     // per-query counts (items of one cell share queries across slices: atomics)
+    if constexpr (CORE) {
+      // the 8 lanes of a query group (threadIdx.x >> 3) hold its 4 queries' counts
+      const int qg = threadIdx.x >> 3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        unsigned c = qc[k][0];
+        c += __shfl_xor_sync(0xffffffffu, c, 1);
+        c += __shfl_xor_sync(0xffffffffu, c, 2);
+        c += __shfl_xor_sync(0xffffffffu, c, 4);
+        const int q = qg + 16 * k;
+        if ((threadIdx.x & 7) == 0 && q < nq && c) atomicAdd(&a.qcount[it.q0 + q], c);
+      }
+    } else {
 #pragma unroll
     for (int g = 0; g < 4; ++g)
 #pragma unroll
@@ -279,10 +370,12 @@ __global__ void __launch_bounds__(kGramThreads, MINB) refine_gram_kernel(RefineA
         const int q = 32 * wq + 8 * g + 2 * col + jj;
         if (row == 0 && q < nq && c) atomicAdd(&a.qcount[it.q0 + q], c);
       }
+    }
     if (threadIdx.x == 0) atomicAdd(&a.ctr->refined, (unsigned long long)nq * (s1 - s0));
   }
   hb.flush(hits, a);
-  flush_stats(a, st_tiles_ref, st_tiles_ref * NCH, 0, 0);
+  if (CORE) st_tiles_ref = 0;  // CUDA-core kernels report no tiles (join.py:328)
+  flush_stats(a, st_tiles_ref, st_tiles_ref * NCH, 0, rechecks);
 }
 
 // Items of <= 64 queries x candidate slices of ~32k (a multiple of 64).
@@ -290,12 +383,12 @@ bool gram_applies(int d_pad, int64_t n, int64_t n_cells) {
   return d_pad >= 12 && n >= int64_t(256) * n_cells;
 }
 
-template <int NCH>
+template <int NCH, bool CORE>
 static void launch_gram_t(const RefineArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(GramSmem<NCH>);
+  const size_t smem = sizeof(GramSmem<NCH, CORE>);
   // 3 CTAs (12 warps, <= 168 registers) per SM while the shared memory allows
   constexpr int kMinBlocks = NCH <= 10 ? 3 : 2;
-  auto kern = refine_gram_kernel<NCH, kMinBlocks>;
+  auto kern = refine_gram_kernel<NCH, kMinBlocks, CORE>;
   TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGramThreads, smem));
@@ -305,25 +398,31 @@ static void launch_gram_t(const RefineArgs& a, cudaStream_t s) {
   TJ_CHECK_LAUNCH();
 }
 
-void launch_refine_gram(const RefineArgs& a, cudaStream_t s) {
+template <bool CORE>
+static void launch_gram_c(const RefineArgs& a, cudaStream_t s) {
   switch (a.nchunks) {
-    case 3: return launch_gram_t<3>(a, s);
-    case 4: return launch_gram_t<4>(a, s);
-    case 5: return launch_gram_t<5>(a, s);
-    case 6: return launch_gram_t<6>(a, s);
-    case 7: return launch_gram_t<7>(a, s);
-    case 8: return launch_gram_t<8>(a, s);
-    case 9: return launch_gram_t<9>(a, s);
-    case 10: return launch_gram_t<10>(a, s);
-    case 11: return launch_gram_t<11>(a, s);
-    case 12: return launch_gram_t<12>(a, s);
-    case 13: return launch_gram_t<13>(a, s);
-    case 14: return launch_gram_t<14>(a, s);
-    case 15: return launch_gram_t<15>(a, s);
-    case 16: return launch_gram_t<16>(a, s);
+    case 3: return launch_gram_t<3, CORE>(a, s);
+    case 4: return launch_gram_t<4, CORE>(a, s);
+    case 5: return launch_gram_t<5, CORE>(a, s);
+    case 6: return launch_gram_t<6, CORE>(a, s);
+    case 7: return launch_gram_t<7, CORE>(a, s);
+    case 8: return launch_gram_t<8, CORE>(a, s);
+    case 9: return launch_gram_t<9, CORE>(a, s);
+    case 10: return launch_gram_t<10, CORE>(a, s);
+    case 11: return launch_gram_t<11, CORE>(a, s);
+    case 12: return launch_gram_t<12, CORE>(a, s);
+    case 13: return launch_gram_t<13, CORE>(a, s);
+    case 14: return launch_gram_t<14, CORE>(a, s);
+    case 15: return launch_gram_t<15, CORE>(a, s);
+    case 16: return launch_gram_t<16, CORE>(a, s);
     default: break;
   }
-  fail(TJ_EINVAL, "Gram DMMA refine is instantiated for 9 <= d <= 64, got d=" + std::to_string(a.d));
+  fail(TJ_EINVAL, "Gram refine is instantiated for 9 <= d <= 64, got d=" + std::to_string(a.d));
+}
+
+void launch_refine_gram(const RefineArgs& a, bool cuda_cores, cudaStream_t s) {
+  if (cuda_cores) launch_gram_c<true>(a, s);
+  else launch_gram_c<false>(a, s);
 }
 
 }  // namespace tj

@@ -442,18 +442,23 @@ def test_lattice_boundary_pairs(kernel, d):
     (1300, 64, 1, 2.759),    # one cell, NCH = 16
     (40000, 12, 1, 0.609),   # > one 32k-candidate slice per item
 ])
-def test_gram_kernel_big_cells(n, d, k_idx, eps):
-    """Big cells at d_pad >= 12 take the CTA-blocked Gram DMMA kernel (refine_gram.cu):
-    its pair set, tile count and candidate count equal the oracle's / the reference formula."""
+@pytest.mark.parametrize("kernel", ["tile", "core_expanded"])
+def test_gram_kernel_big_cells(n, d, k_idx, eps, kernel):
+    """Big cells at d_pad >= 12 take the CTA-blocked Gram kernels (refine_gram.cu): DMMA
+    for "tile", the same blocking in DFMA for "core_expanded".  Pair set, tile count and
+    candidate count equal the oracle's / the reference formula."""
     ds = generate(GenSpec("uniform", n, d, seed=n + d))
-    r = self_join(ds, JoinConfig(epsilon=eps, k_idx=k_idx))
+    r = self_join(ds, JoinConfig(epsilon=eps, k_idx=k_idx, kernel=kernel))
     assert_oracle_equal(r, ds, eps, k_idx=k_idx)
     _, cstart, _, cand = oracle.grid(ds, eps, k_idx)
     nq = np.diff(cstart)
     assert r.stats.candidates_refined == int(np.sum(nq * cand))
-    tiles = int(np.sum(-(-nq // 8) * -(-cand // 8)))
-    assert r.stats.tiles_processed == tiles
-    assert r.stats.chunks_executed + r.stats.chunks_skipped == tiles * ((d + 3) // 4)
+    if kernel == "tile":
+        tiles = int(np.sum(-(-nq // 8) * -(-cand // 8)))
+        assert r.stats.tiles_processed == tiles
+        assert r.stats.chunks_executed + r.stats.chunks_skipped == tiles * ((d + 3) // 4)
+    else:
+        assert r.stats.tiles_processed == 0
 
 
 # ------------------------------------------------------ output-budget batcher
