@@ -108,8 +108,8 @@ int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int6
  * ctx result buffer.  Asynchronous. */
 int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
               int64_t cell_end, void* stream);
-/* Low-d DMMA symmetric join (default on; TJ_SYMMETRIC=0 in the environment turns
- * the default off): the refine covers each cell's candidates from the cell itself
+/* Low-d DMMA symmetric join (default off; TJ_SYMMETRIC=1 in the environment turns
+ * the default on): the refine covers each cell's candidates from the cell itself
  * on, so every pair of neighbour cells is multiplied once, and the rows of a
  * cell's queries take their pairs with earlier cells from those cells' hit masks.
  * It needs every earlier cell refined in the same result set: callers refining a

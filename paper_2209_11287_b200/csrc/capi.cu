@@ -124,8 +124,8 @@ int tj_ctx_create(int device, tj_ctx** out) {
     TJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     tj_ctx* c = new tj_ctx();
     c->device = device;
-    const char* sym = std::getenv("TJ_SYMMETRIC");  // low-d symmetric join (default on)
-    c->symmetric = !(sym && sym[0] == '0');
+    const char* sym = std::getenv("TJ_SYMMETRIC");  // low-d symmetric join (default off)
+    c->symmetric = sym && sym[0] == '1';
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
     cudaEventCreate(&c->ev2);

@@ -377,10 +377,11 @@ class DeviceJoin:
         if cell_range is not None:
             lo, hi = cell_range
             batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
-        # the low-d symmetric join (TJ_SYMMETRIC=0 turns it off) reads every earlier
-        # cell's masks: for a cell range past cell 0 (a multi-GPU shard) the earlier
-        # cells -- the shard's halo -- are refined for their masks only, below
-        symmetric = os.environ.get("TJ_SYMMETRIC", "1") != "0"
+        # the low-d symmetric join (TJ_SYMMETRIC=1; measured slower on the device
+        # step) reads every earlier cell's masks: for a cell range
+        # past cell 0 (a multi-GPU shard) the earlier cells -- the shard's halo --
+        # are refined for their masks only, below
+        symmetric = os.environ.get("TJ_SYMMETRIC", "0") == "1"
         self.ctx.set_symmetric(symmetric)
         appends = self.appends_pairs()
         if appends and batches:

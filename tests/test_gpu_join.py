@@ -510,3 +510,52 @@ def test_pair_estimate_is_close_for_uniform_data():
         assert total <= est <= 2 * total, (kernel, total, est)
         r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel))
         assert r.total_pairs == total
+
+
+# ------------------------------------------------ low-d symmetric join (option)
+@pytest.mark.parametrize("case", _sweep_cases()[::3], ids=lambda c: f"{c['dist'][:3]}-n{c['n']}-d{c['d']}-S{c['target']}")
+def test_symmetric_join_matches_reference(case, monkeypatch):
+    """TJ_SYMMETRIC=1: every neighbour-cell pair multiplied once, rows completed from
+    the earlier cells' masks -- the same pair set (golden SHA-256) in one batch and in
+    many, through both the device finalize and the chunked host pipeline."""
+    monkeypatch.setenv("TJ_SYMMETRIC", "1")
+    ds = generate(GenSpec(case["dist"], case["n"], case["d"], seed=case["seed"]))
+    for batch in (None, 64):
+        r = self_join(ds, JoinConfig(epsilon=case["eps"], batch_size=batch))
+        assert r.total_pairs == case["pairs"]
+        assert sha_pairs(r.pairs) == case["sha_pairs"]
+        if case["d"] <= 4:
+            assert r.stats.tiles_processed == case["tiles"]
+
+
+@pytest.mark.parametrize("d", [2, 3, 4])
+def test_symmetric_join_shard_ranges(d, monkeypatch):
+    """A cell range past cell 0 (multi-GPU shard): the earlier cells are refined for
+    their masks only (tj_refine_masks); the range's rows equal the full join's."""
+    from paper_2209_11287_b200.join import DeviceJoin
+
+    monkeypatch.setenv("TJ_SYMMETRIC", "1")
+    ds = generate(GenSpec("uniform", 20_000, d, seed=d))
+    eps = {2: 0.01, 3: 0.04, 4: 0.08}[d]
+    full_off, full_nb = oracle.join_csr(ds, eps)
+    job = DeviceJoin(ds, JoinConfig(epsilon=eps))
+    info = job.build()
+    lo, hi = info.n_cells // 3, 2 * info.n_cells // 3
+    job.refine(cell_range=(lo, hi))
+    off, nb = job.finalize_fetch()
+    _, cstart, _, _ = oracle.grid(ds, eps)
+    order = oracle.grid(ds, eps)[0]
+    ids = order[cstart[lo]: cstart[hi]].astype(np.int64)
+    for i in ids[:: max(1, len(ids) // 300)]:
+        assert np.array_equal(nb[off[i]: off[i + 1]].astype(np.int64),
+                              full_nb[full_off[i]: full_off[i + 1]].astype(np.int64)), i
+    assert int(off[-1]) == int(sum(full_off[i + 1] - full_off[i] for i in ids))
+
+
+def test_symmetric_join_full_size_c2(monkeypatch):
+    from test_gpu_parity import FULL, _check, device_digest
+
+    if "c2" not in FULL:
+        pytest.skip("oracle digest not generated")
+    monkeypatch.setenv("TJ_SYMMETRIC", "1")
+    _check(device_digest(FULL["c2"], "tile"), FULL["c2"])
