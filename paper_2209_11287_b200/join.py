@@ -223,12 +223,14 @@ def resolve_k_idx(config: JoinConfig, d: int) -> int:
     return k_idx
 
 
-# Refine-kernel throughput measured on one B200 (FP64 TFLOP/s, 2*d flops per
-# candidate pair; profiles/r1e/sweep.jsonl): (d, DMMA tile, CUDA-core).  The
-# DMMA formulation wins at every measured d; above the DMMA instantiation
-# (d > 64) only the CUDA-core kernel exists.
-MEASURED_KERNEL_TFLOPS = ((2, 4.44, 1.39), (4, 9.44, 4.71), (8, 13.17, 6.38), (16, 16.78, 6.36),
-                          (32, 19.09, 5.36))
+# Refine-kernel throughput measured on one B200, round 2 (FP64 TFLOP/s, 2*d flops
+# per candidate pair, short_circuit off; profiles/r2i/kncu, profiles/r2i/sweep_core.jsonl,
+# profiles/r2g/sweep_hd.jsonl): (d, DMMA tile, best CUDA-core variant).  The CUDA-core
+# kernels are issue-bound (ncu: 72-90 % issue-active, FP64 pipe 25-54 %); the DMMA
+# formulation does 256 FMAs per instruction and wins at every measured d.  Above
+# the DMMA instantiation (d > 64) only the CUDA-core kernel exists.
+MEASURED_KERNEL_TFLOPS = ((2, 4.44, 1.39), (4, 9.64, 4.72), (8, 17.3, 6.38), (16, 23.8, 4.92),
+                          (32, 27.0, 5.36), (64, 27.9, 3.2))
 DMMA_MAX_DIM = 64
 
 # JoinConfig.kernel -> tj_refine kernel code.  'tile' and 'scalar' are the
