@@ -95,7 +95,6 @@ def rank_step(plan, r, G):
     ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b, out=local, gid=gid)
     torch.cuda.synchronize()
     t.append(ev())
-    t.append(ev())
     job = DeviceJoin(Dataset._wrap(np.empty((n_local, coords.shape[1])), d), cfg)
     job.build(local[:n_local])
     cb, ce = ctx.shard_cell_range(pdims, plan.origin, plan.span, lo_b, hi_b)
