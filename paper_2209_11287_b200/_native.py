@@ -77,6 +77,8 @@ SIGNATURES = {
     "tj_shard_histogram": (_i32, [_vp, _vp, _i64, _i64, _i32, _f64, _vp, _vp, _vp, _vp]),
     "tj_shard_select": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _f64, _vp, _vp, _i64, _i64,
                                _vp, _i64, _vp, _i64, _i64, ctypes.POINTER(_i64), _vp]),
+    "tj_shard_route": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _f64, _vp, _vp, _vp, _vp, _i32,
+                              _vp, _vp, _i64, _vp, _i64, _i64, _vp]),
     "tj_shard_cell_range": (_i32, [_vp, _i32, _vp, _vp, _i64, _i64, ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64)]),
     "tj_remap_ids": (_i32, [_vp, _vp, _i64, _vp, _vp]),
@@ -337,6 +339,25 @@ class Context:
             int(out.shape[0]) if out is not None else 0, ctypes.byref(sel),
             self.stream().cuda_stream))
         return int(sel.value)
+
+    def shard_route(self, coords, n: int, d: int, pdims: int, eps: float, origin, span, ranges,
+                    counts=None, out=None, gid=None, gid_base: int = 0):
+        """Count (out None) or write the rows each rank needs (tj_shard_route)."""
+        import numpy as np
+
+        o, sp = self._bins(pdims, origin, span)
+        lo = np.ascontiguousarray([r[0] for r in ranges], dtype=np.int64)
+        hi = np.ascontiguousarray([r[1] for r in ranges], dtype=np.int64)
+        cnt = (np.zeros(len(ranges), np.int64) if counts is None
+               else np.ascontiguousarray(counts, dtype=np.int64))
+        self._check(self.lib.tj_shard_route(
+            self.handle, coords.data_ptr() if n else None, int(n), int(coords.stride(0)), int(d),
+            int(pdims), float(eps), o.ctypes.data, sp.ctypes.data, lo.ctypes.data, hi.ctypes.data,
+            len(ranges), cnt.ctypes.data, out.data_ptr() if out is not None else None,
+            int(out.stride(0)) if out is not None else 0,
+            gid.data_ptr() if gid is not None else None, int(gid_base),
+            int(out.shape[0]) if out is not None else 0, self.stream().cuda_stream))
+        return [int(v) for v in cnt]
 
     def shard_cell_range(self, pdims: int, origin, span, own_lo: int, own_hi: int):
         o, sp = self._bins(pdims, origin, span)

@@ -828,6 +828,21 @@ int tj_shard_select(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, in
   });
 }
 
+int tj_shard_route(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t d,
+                   int32_t pdims, double eps, const int64_t* origin, const int64_t* span,
+                   const int64_t* own_lo, const int64_t* own_hi, int32_t ranks, int64_t* counts,
+                   double* out, int64_t ld_out, uint32_t* gid, int64_t gid_base, int64_t capacity,
+                   void* stream) {
+  if (!ctx || !counts || !own_lo || !own_hi || ranks < 1 || ranks > 1024) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    check_bins(pdims, origin, span);
+    if (n > 0 && (!coords || ld < d || d < pdims)) fail(TJ_EINVAL, "need coords, ld >= d >= pdims");
+    if (out && (!gid || ld_out < d)) fail(TJ_EINVAL, "need gid and ld_out >= d with out");
+    shard_route(ctx, coords, n, ld, d, pdims, eps, origin, span, own_lo, own_hi, ranks, counts, out,
+                ld_out, gid, gid_base, capacity, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int tj_shard_cell_range(tj_ctx* ctx, int32_t pdims, const int64_t* origin, const int64_t* span,
                         int64_t own_lo, int64_t own_hi, int64_t* cell_begin, int64_t* cell_end) {
   if (!ctx || !cell_begin || !cell_end) return TJ_EINVAL;

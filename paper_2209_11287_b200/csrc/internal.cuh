@@ -203,6 +203,10 @@ int64_t shard_select(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d,
                      double eps, const int64_t* origin, const int64_t* span, int64_t own_lo,
                      int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid, int64_t gid_base,
                      int64_t capacity, cudaStream_t s);
+void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int pdims, double eps,
+                 const int64_t* origin, const int64_t* span, const int64_t* lo, const int64_t* hi,
+                 int G, int64_t* counts, double* out, int64_t ld_out, uint32_t* gid,
+                 int64_t gid_base, int64_t capacity, cudaStream_t s);
 void shard_cell_range(tj_ctx* ctx, int pdims, const int64_t* origin, const int64_t* span,
                       int64_t own_lo, int64_t own_hi, int64_t* begin, int64_t* end, cudaStream_t s);
 void shard_remap_ids(uint32_t* ids, int64_t m, const uint32_t* gid, cudaStream_t s);

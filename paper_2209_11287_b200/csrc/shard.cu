@@ -157,6 +157,25 @@ struct NoStore {
   __device__ void operator()(int64_t, int64_t) const {}
 };
 
+// Points of this rank's rows needed by each of G ranks (owned bins + halo).
+__global__ void route_count_kernel(const double* __restrict__ x, int64_t n, int64_t ld, Bins b,
+                                   const long long* __restrict__ lo, const long long* __restrict__ hi,
+                                   int G, unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int s_cnt[];
+  for (int r = threadIdx.x; r < G; r += blockDim.x) s_cnt[r] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    long long b0, b1;
+    point_bins(x + i * ld, b, b0, b1);
+    for (int r = 0; r < G; ++r)
+      if (bin_needed(b0, b1, b, lo[r], hi[r])) atomicAdd(&s_cnt[r], 1u);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < G; r += blockDim.x)
+    if (s_cnt[r]) atomicAdd(&counts[r], (unsigned long long)s_cnt[r]);
+}
+
 // First cell c of the local grid whose bin index is >= target (cells are
 // lexicographic, so their prefix bins are non-decreasing).
 __global__ void cell_bound_kernel(const double* __restrict__ P, const int64_t* __restrict__ cell_start,
@@ -271,6 +290,48 @@ int64_t shard_select(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d,
   TJ_CUDA(cudaStreamSynchronize(s));
   if (out && total > capacity) fail(TJ_ECAPACITY, "shard_select: output capacity too small");
   return total;
+}
+
+void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int pdims, double eps,
+                 const int64_t* origin, const int64_t* span, const int64_t* lo, const int64_t* hi,
+                 int G, int64_t* counts, double* out, int64_t ld_out, uint32_t* gid,
+                 int64_t gid_base, int64_t capacity, cudaStream_t s) {
+  const Bins b = make_bins(pdims, eps, origin, span);
+  if (!out) {  // counts only: one pass over the rows, one read-back
+    ctx->tmp64.ensure(sizeof(long long) * (2 * G) + sizeof(unsigned long long) * G + 64, s);
+    long long* dlo = reinterpret_cast<long long*>(ctx->tmp64.ptr);
+    long long* dhi = dlo + G;
+    unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(dhi + G);
+    std::vector<long long> hlh(2 * G);
+    for (int r = 0; r < G; ++r) {
+      hlh[r] = lo[r];
+      hlh[G + r] = hi[r];
+    }
+    TJ_CUDA(cudaMemcpyAsync(dlo, hlh.data(), sizeof(long long) * 2 * G, cudaMemcpyHostToDevice, s));
+    TJ_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * G, s));
+    if (n > 0) {
+      route_count_kernel<<<grid_for(n, 256), 256, sizeof(unsigned) * G, s>>>(x, n, ld, b, dlo, dhi,
+                                                                            G, dcnt);
+      TJ_CHECK_LAUNCH();
+    }
+    std::vector<unsigned long long> hc(G);
+    TJ_CUDA(cudaMemcpyAsync(hc.data(), dcnt, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost, s));
+    TJ_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < G; ++r) counts[r] = int64_t(hc[r]);
+    return;
+  }
+  // write: destination r's rows at [sum(counts[<r]), ...), stable (no read-back)
+  int64_t off = 0;
+  for (int r = 0; r < G; ++r) {
+    if (off + counts[r] > capacity) fail(TJ_ECAPACITY, "shard_route: output capacity too small");
+    if (counts[r] > 0) {
+      const HaloPred pred{x, ld, b, lo[r], hi[r]};
+      ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+      scan_exclusive(HaloCount{pred},
+                     HaloWrite{pred, d, out + off * ld_out, ld_out, gid + off, gid_base}, n, sc, s);
+    }
+    off += counts[r];
+  }
 }
 
 void shard_cell_range(tj_ctx* ctx, int pdims, const int64_t* origin, const int64_t* span,

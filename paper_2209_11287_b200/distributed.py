@@ -13,7 +13,7 @@ batch's cells (join.py:184-197) -- with the strong layout of SURVEY.md 8(e):
    bin ranges of equal cost -- contiguous cell ranges of the reference order;
 4. every rank routes its own rows to the ranks that need them -- a point goes to
    the owner of its bin and to the ranks whose bins are in its one-cell halo
-   (stable compaction per destination on the device, tj_shard_select) -- and
+   (one counting pass + a stable compaction per destination, tj_shard_route) -- and
    one all-to-all (NCCL over NVLink) delivers each rank its bins' points plus
    its halo, in global id order;
 5. each rank builds the grid over those points, refines only its owned cells
@@ -210,18 +210,15 @@ def exchange_points(ctx, rows, gid_base: int, d: int, eps: float, plan: ShardPla
     world = dist.get_world_size(group)
     n_my, width = rows.shape[0], rows.shape[1]
     pdims = plan.pdims
-    counts = [ctx.shard_select(rows, n_my, d, pdims, eps, plan.origin, plan.span, lo, hi)
-              if n_my else 0 for lo, hi in plan.ranges]
-    total = sum(counts)
     dev = rows.device
+    # one counting pass over the rows for every destination, then the stable writes
+    counts = ctx.shard_route(rows, n_my, d, pdims, eps, plan.origin, plan.span, plan.ranges)
+    total = sum(counts)
     send = torch.empty((max(total, 1), width), dtype=torch.float64, device=dev)
     send_gid = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-    off = 0
-    for (lo, hi), c in zip(plan.ranges, counts):
-        if c:
-            ctx.shard_select(rows, n_my, d, pdims, eps, plan.origin, plan.span, lo, hi,
-                             out=send[off: off + c], gid=send_gid[off: off + c], gid_base=gid_base)
-        off += c
+    if total:
+        ctx.shard_route(rows, n_my, d, pdims, eps, plan.origin, plan.span, plan.ranges,
+                        counts=counts, out=send, gid=send_gid, gid_base=gid_base)
     cdev = dev if dist.get_backend(group) != "gloo" else torch.device("cpu")
     sc = torch.tensor(counts, dtype=torch.int64, device=cdev)
     rc = torch.empty_like(sc)

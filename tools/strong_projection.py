@@ -77,16 +77,11 @@ def rank_step(plan, r, G):
     per = -(-n // G)
     sl = coords[r * per: min(n, (r + 1) * per)]
     t = [ev()]
-    cnts = [ctx.shard_select(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, a_, b_)
-            for a_, b_ in plan.ranges]
+    cnts = ctx.shard_route(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, plan.ranges)
     send = torch.empty((max(sum(cnts), 1), coords.shape[1]), dtype=torch.float64, device=dev)
     sgid = torch.empty(max(sum(cnts), 1), dtype=torch.int32, device=dev)
-    off = 0
-    for (a_, b_), c_ in zip(plan.ranges, cnts):
-        if c_:
-            ctx.shard_select(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, a_, b_,
-                             out=send[off: off + c_], gid=sgid[off: off + c_], gid_base=r * per)
-        off += c_
+    ctx.shard_route(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, plan.ranges,
+                    counts=cnts, out=send, gid=sgid, gid_base=r * per)
     t.append(ev())
     # what this rank receives (the same set, in global id order)
     n_local = ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b)
