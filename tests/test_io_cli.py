@@ -201,3 +201,45 @@ def test_cli_join_verify_bench(tmp_path, capsys):
                      "--report", str(brep)]) == 0
     rows = cli.load_report(brep)["rows"]
     assert len(rows) == 4 and all(r["fp64_tflops"] > 0 for r in rows)
+
+
+@pytest.mark.gpu
+def test_cli_join_large_pinned_input(tmp_path, capsys):
+    """an input above the 1 MB registration threshold read into pinned memory
+    (read_dataset(pinned=True)) must not trip a stale CUDA error on re-registration;
+    joins of views and repeated joins of the same pinned buffer stay exact."""
+    pts = tmp_path / "big.bin"
+    assert cli.main(["generate", "--dist", "uniform", "--n", "200000", "--d", "3", "--out",
+                     str(pts)]) == 0
+    capsys.readouterr()
+    rep = tmp_path / "r.json"
+    for _ in range(2):
+        assert cli.main(["join", "--input", str(pts), "--epsilon", "0.01", "--report",
+                         str(rep)]) == 0
+    ds = read_dataset(pts, pinned=True)
+    off, nb = oracle.join_csr(ds, 0.01)
+    assert cli.load_report(rep)["result"]["total_pairs"] == int(off[-1])
+    r = self_join(ds, JoinConfig(epsilon=0.01))
+    assert csr_equal(r.offsets, r.neighbors, off, nb)
+    half = ds.coords[: ds.n // 2]  # a view into the same pinned allocation
+    from paper_2209_11287_b200 import Dataset
+
+    r2 = self_join(Dataset(half[:, :3]), JoinConfig(epsilon=0.01))
+    o2, n2 = oracle.join_csr(Dataset(half[:, :3]), 0.01)
+    assert csr_equal(r2.offsets, r2.neighbors, o2, n2)
+
+
+@pytest.mark.gpu
+def test_pairs_expansion_is_fast():
+    """JoinResult.pairs of config 2 (1.3e8 pairs) within a few hundred ms."""
+    import time
+
+    ds = generate(GenSpec("uniform", 2_000_000, 4, seed=0))
+    r = self_join(ds, JoinConfig(epsilon=0.051306))
+    t = time.perf_counter()
+    p = r.pairs
+    dt = time.perf_counter() - t
+    assert p.shape == (r.total_pairs, 2)
+    assert np.array_equal(p[:, 1], r.neighbors.astype(np.int64))
+    print(f"pairs expansion {dt * 1e3:.1f} ms for {r.total_pairs} pairs")
+    assert dt < 1.0
