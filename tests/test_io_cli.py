@@ -224,8 +224,9 @@ def test_cli_join_large_pinned_input(tmp_path, capsys):
     half = ds.coords[: ds.n // 2]  # a view into the same pinned allocation
     from paper_2209_11287_b200 import Dataset
 
-    r2 = self_join(Dataset(half[:, :3]), JoinConfig(epsilon=0.01))
-    o2, n2 = oracle.join_csr(Dataset(half[:, :3]), 0.01)
+    view = Dataset._wrap(half, 3)
+    r2 = self_join(view, JoinConfig(epsilon=0.01))
+    o2, n2 = oracle.join_csr(view, 0.01)
     assert csr_equal(r2.offsets, r2.neighbors, o2, n2)
 
 
