@@ -108,6 +108,12 @@ int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int6
  * ctx result buffer.  Asynchronous. */
 int tj_refine(tj_ctx* ctx, int32_t kernel, int32_t short_circuit, int64_t cell_begin,
               int64_t cell_end, void* stream);
+/* Neighbour ids of the canonical output written as id_map[original id] (device
+ * uint32[n] of the current grid, caller-owned, alive until the rows are built;
+ * NULL = the original ids).  A multi-GPU shard passes its local -> global id map
+ * (monotone, so rows stay sorted) and skips a remap pass over the rows.  Reset by
+ * tj_build_grid. */
+int tj_set_output_ids(tj_ctx* ctx, const uint32_t* id_map);
 /* Low-d DMMA symmetric join (default off; TJ_SYMMETRIC=1 in the environment turns
  * the default on): the refine covers each cell's candidates from the cell itself
  * on, so every pair of neighbour cells is multiplied once, and the rows of a

@@ -55,6 +55,7 @@ SIGNATURES = {
     "tj_reserve_results": (_i32, [_vp, _i64]),
     "tj_checkpoint_results": (_i32, [_vp, _vp]),
     "tj_set_symmetric": (_i32, [_vp, _i32]),
+    "tj_set_output_ids": (_i32, [_vp, _vp]),
     "tj_refine_masks": (_i32, [_vp, _i32, _i32, _i64, _i64, _vp]),
     "tj_estimate_pairs": (_i32, [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64,
                                  ctypes.POINTER(_f64), _vp]),
@@ -219,6 +220,10 @@ class Context:
         s = stream or self.stream()
         self._check(self.lib.tj_refine_masks(self.handle, kernel, int(bool(short_circuit)),
                                              cell_begin, cell_end, s.cuda_stream))
+
+    def set_output_ids(self, id_map):
+        self._check(self.lib.tj_set_output_ids(self.handle,
+                                               id_map.data_ptr() if id_map is not None else None))
 
     def set_symmetric(self, on: bool):
         self._check(self.lib.tj_set_symmetric(self.handle, int(bool(on))))

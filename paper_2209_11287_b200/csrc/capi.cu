@@ -146,7 +146,7 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
                     &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell,
                     &ctx->fwd,      &ctx->bt_start,  &ctx->bt,       &ctx->chunk_key,
-                    &ctx->bt_desc};
+                    &ctx->bt_desc,  &ctx->nid};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -182,6 +182,8 @@ int tj_build_grid(tj_ctx* ctx, const double* coords, int64_t n, int32_t d, int64
     if (ld < d) fail(TJ_EINVAL, "ld must be >= d");
     ctx->masks_ready = false;
     ctx->id_maps_ready = false;
+    ctx->out_ids = nullptr;
+    ctx->nid_ready = false;
     build_grid(ctx, coords, n, d, ld, k_idx, eps, s);
     zero_results(ctx, s);
     ctx->last_stream = s;
@@ -536,6 +538,15 @@ int tj_estimate_pairs(tj_ctx* ctx, int32_t kernel, int64_t cell_begin, int64_t c
     ctx->ctr_valid = false;
     const double refined = double(after.refined - before.refined);
     *pairs_per_candidate = refined > 0 ? double(after.pairs - before.pairs) / refined : 0.0;
+  });
+}
+
+int tj_set_output_ids(tj_ctx* ctx, const uint32_t* id_map) {
+  if (!ctx) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    require_grid(ctx);
+    ctx->out_ids = id_map;
+    ctx->nid_ready = false;
   });
 }
 

@@ -31,14 +31,14 @@ __global__ void counts_to_orig_kernel(const uint32_t* __restrict__ qcount,
 // Pair path: (query position, candidate position) -> the query's row in cell
 // (position) order through a per-row atomic cursor; ids are original ids.
 __global__ void scatter_pairs_kernel(const uint2* __restrict__ pairs, int64_t total,
-                                     const uint32_t* __restrict__ perm,
+                                     const uint32_t* __restrict__ nid,
                                      const int64_t* __restrict__ pos_off,
                                      uint32_t* __restrict__ fill, uint32_t* __restrict__ rows) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const uint2 pr = pairs[e];
     const uint32_t slot = atomicAdd(&fill[pr.x], 1u);
-    rows[pos_off[pr.x] + slot] = perm[pr.y];
+    rows[pos_off[pr.x] + slot] = nid[pr.y];
   }
 }
 
@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
                      const uint32_t* __restrict__ run_off, const int64_t* __restrict__ cell_cand,
                      int64_t n_cells, const uint32_t* __restrict__ win_cell,
                      const uint32_t* __restrict__ qcount, const uint32_t* __restrict__ perm,
+                     const uint32_t* __restrict__ nid,
                      const int64_t* __restrict__ offsets, int64_t n, uint32_t* __restrict__ nbr,
                      uint32_t* __restrict__ long_rows, unsigned long long* n_long, RowList rl,
                      SymTables sym) {
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
         uint32_t v[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          v[u] = i0 + u < len ? __ldg(perm + col[(i0 + u) * kPoolLd]) : 0u;
+          v[u] = i0 + u < len ? __ldg(nid + col[(i0 + u) * kPoolLd]) : 0u;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
           if (i0 + u < len) col[(i0 + u) * kPoolLd] = v[u];
@@ -694,6 +695,7 @@ __global__ void __launch_bounds__(256)
                      const int64_t* __restrict__ cell_runs, const uint2* __restrict__ runs,
                      const uint32_t* __restrict__ run_off, const int64_t* __restrict__ cell_cand,
                      int64_t n_cells, const uint32_t* __restrict__ perm,
+                     const uint32_t* __restrict__ nid,
                      const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
                      const uint32_t* __restrict__ long_rows, const unsigned long long* n_long,
                      uint32_t* __restrict__ big_rows, unsigned long long* n_big, SymTables sym) {
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(256)
     __syncwarp();
     const int64_t rb = cell_runs[c];
     const int nr = int(cell_runs[c + 1] - rb);
-    for (int e = lane; e < base; e += 32) row[e] = perm[run_position(runs, run_off, rb, nr, row[e])];
+    for (int e = lane; e < base; e += 32) row[e] = nid[run_position(runs, run_off, rb, nr, row[e])];
     // symmetric join: the pairs with earlier neighbour cells (rare long rows: one lane)
     if (sym.fwd && lane == 0) {
       int at = base;
@@ -746,7 +748,7 @@ __global__ void __launch_bounds__(256)
                           while (bits) {
                             const int j = __ffs(bits) - 1;
                             bits &= bits - 1u;
-                            row[at++] = perm[qbase + cand_bit_query(j)];
+                            row[at++] = nid[qbase + cand_bit_query(j)];
                           }
                         });
     }
@@ -902,6 +904,32 @@ __global__ void pcell_kernel(const int64_t* __restrict__ cell_start, int64_t n_c
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps)
     for (int64_t p = cell_start[c] + lane_id(); p < cell_start[c + 1]; p += 32) pcell[p] = uint32_t(c);
+}
+
+__global__ void compose_ids_kernel(const uint32_t* __restrict__ perm,
+                                   const uint32_t* __restrict__ id_map, int64_t n,
+                                   uint32_t* __restrict__ out) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
+       p += int64_t(gridDim.x) * blockDim.x)
+    out[p] = id_map[perm[p]];
+}
+
+// Id written for a neighbour at cell-ordered position p: the original id perm[p],
+// or id_map[perm[p]] when the caller set an output id map (tj_set_output_ids: a
+// multi-GPU shard writes global ids straight away, no remap pass over the rows).
+static const uint32_t* neighbour_ids(tj_ctx* ctx, cudaStream_t s) {
+  if (!ctx->out_ids) return ctx->perm.as<uint32_t>();
+  if (!ctx->nid_ready) {
+    const int64_t n = ctx->g.n;
+    ctx->nid.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1), s);
+    compose_ids_kernel<<<unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256),
+                                                                          kNumSMs * 16))),
+                         256, 0, s>>>(ctx->perm.as<uint32_t>(), ctx->out_ids, n,
+                                      ctx->nid.as<uint32_t>());
+    TJ_CHECK_LAUNCH();
+    ctx->nid_ready = true;
+  }
+  return ctx->nid.as<uint32_t>();
 }
 
 static SymTables sym_tables(const tj_ctx* ctx) {
@@ -1100,15 +1128,15 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
         ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
         ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
-        offsets, n, nbr, long_rows, nbig + 2, rl, sym_tables(ctx));
+        neighbour_ids(ctx, s), offsets, n, nbr, long_rows, nbig + 2, rl, sym_tables(ctx));
     TJ_CHECK_LAUNCH();
   }
   long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
       ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
-      ctx->perm.as<uint32_t>(), offsets, nbr, long_rows, nbig + 2, fill, nbig,
-      sym_tables(ctx));
+      ctx->perm.as<uint32_t>(), neighbour_ids(ctx, s), offsets, nbr, long_rows, nbig + 2, fill,
+      nbig, sym_tables(ctx));
   TJ_CHECK_LAUNCH();
   if (max_mask_row > kWarpSortMax)
     sort_big_rows(ctx, const_cast<int64_t*>(offsets), nbr, fill, nbig, s);
@@ -1162,7 +1190,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
           ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
           ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc,
           ctx->win_cell.as<uint32_t>(), ctx->qcount.as<uint32_t>(), ctx->perm.as<uint32_t>(),
-          offsets, n, nbr, long_rows, nbig + 2, RowList{}, sym_tables(ctx));
+          neighbour_ids(ctx, s), offsets, n, nbr, long_rows, nbig + 2, RowList{}, sym_tables(ctx));
       TJ_CHECK_LAUNCH();
       TJ_CUDA(cudaEventRecord(ctx->ev3, s));
       ctx->have_emit_timing = true;
@@ -1171,7 +1199,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
         ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc, ctx->perm.as<uint32_t>(),
-        offsets, nbr, long_rows, nbig + 2, fill, nbig, sym_tables(ctx));
+        neighbour_ids(ctx, s), offsets, nbr, long_rows, nbig + 2, fill, nbig, sym_tables(ctx));
     TJ_CHECK_LAUNCH();
   } else {
     // pair path: rows in cell (position) order first, then sorted into place
@@ -1184,7 +1212,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     uint32_t* rows = ctx->rows_tmp.as<uint32_t>();
     TJ_CUDA(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, s));
     scatter_pairs_kernel<<<blocks_for(n_pairs, 256), 256, 0, s>>>(
-        ctx->pairs.as<uint2>(), n_pairs, ctx->perm.as<uint32_t>(), pos_off, fill, rows);
+        ctx->pairs.as<uint2>(), n_pairs, neighbour_ids(ctx, s), pos_off, fill, rows);
     TJ_CHECK_LAUNCH();
     const size_t smem = sizeof(uint32_t) * kPoolSlots * kPoolLd * kSortWarps;
     TJ_CUDA(cudaFuncSetAttribute(sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -129,6 +129,10 @@ struct tj_ctx {
   tj::DevBuf pairs, qcount, counters, fill, masks, cell_mbase, win_cell;
   // low-d symmetric join: per-cell forward offset, backward-cell table (CSR by cell)
   tj::DevBuf fwd, bt_start, bt, bt_desc;
+  // output id map (tj_set_output_ids): neighbour ids written as out_ids[original id]
+  const uint32_t* out_ids = nullptr;
+  tj::DevBuf nid;
+  bool nid_ready = false;
   bool symmetric = true;
   tj::DevBuf pos_off, rows_tmp;  // finalize: rows in cell (position) order before the sort
   tj::DevBuf ipos, pcell;        // id-range position lists (2 x n: sort ping-pong), position -> cell

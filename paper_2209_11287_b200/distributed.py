@@ -17,8 +17,9 @@ batch's cells (join.py:184-197) -- with the strong layout of SURVEY.md 8(e):
    one all-to-all (NCCL over NVLink) delivers each rank its bins' points plus
    its halo, in global id order;
 5. each rank builds the grid over those points, refines only its owned cells
-   (tj_shard_cell_range) and emits its canonical CSR rows; local ids are
-   monotone in global ids, so rows stay sorted after tj_remap_ids;
+   (tj_shard_cell_range) and emits its canonical CSR rows with global neighbour
+   ids (tj_set_output_ids: local ids are monotone in global ids, so rows stay
+   sorted);
 6. global row offsets: each rank scatters its row counts to global ids
    (tj_scatter_counts), one SUM all-reduce of n int32 counts, one scan.
 The pair set then sits on the devices, each rank holding its rows and every
@@ -298,8 +299,8 @@ def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> Sh
         mark("index")
         pairs = job.refine(cell_range=(cb, ce))
         mark("refine")
+        ctx.set_output_ids(gid)  # rows carry global neighbour ids (gid is monotone)
         loff, lnbr = job.finalize()
-        ctx.remap_ids(lnbr, pairs, gid)
     else:
         cb = ce = 0
         loff = torch.zeros(1, dtype=torch.int64, device=dev)

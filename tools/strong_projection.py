@@ -96,8 +96,8 @@ def rank_step(plan, r, G):
     t.append(ev())
     pairs = job.refine(cell_range=(cb, ce))
     t.append(ev())
+    ctx.set_output_ids(gid)
     loff, lnbr = job.finalize()
-    ctx.remap_ids(lnbr, pairs, gid)
     counts = torch.zeros(n, dtype=torch.int32, device=dev)
     ctx.scatter_counts(loff, n_local, gid, counts)
     goff = torch.empty(n + 1, dtype=torch.int64, device=dev)
