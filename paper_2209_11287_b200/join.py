@@ -380,7 +380,7 @@ class DeviceJoin:
             lo, hi = cell_range
             batches = [(max(a, lo), min(b, hi)) for a, b in batches if min(b, hi) > max(a, lo)]
         # the low-d symmetric join (TJ_SYMMETRIC=1; measured slower on the device
-        # step, DESIGN.md 3.7) reads every earlier cell's masks: for a cell range
+        # step, DESIGN.md 5.5) reads every earlier cell's masks: for a cell range
         # past cell 0 (a multi-GPU shard) the earlier cells -- the shard's halo --
         # are refined for their masks only, below
         symmetric = os.environ.get("TJ_SYMMETRIC", "0") == "1"
