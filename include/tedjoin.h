@@ -262,10 +262,11 @@ int tj_shard_select(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, in
                     int32_t pdims, double eps, const int64_t* origin, const int64_t* span,
                     int64_t own_lo, int64_t own_hi, double* out, int64_t ld_out, uint32_t* gid,
                     int64_t gid_base, int64_t capacity, int64_t* selected, void* stream);
-/* Route this rank's rows to `ranks` ranks (rank r owns bins [own_lo[r], own_hi[r]]):
- * a row goes to every rank whose bins or one-cell halo hold it.  out == NULL: one
- * pass, counts[r] = rows for rank r (host int64[ranks]; synchronous).  Otherwise
- * (counts from that call): the rows for rank r, stably compacted, at row
+/* Route this rank's rows to `ranks` (<= 64) ranks (rank r owns bins [own_lo[r],
+ * own_hi[r]]): a row goes to every rank whose bins or one-cell halo hold it.
+ * out == NULL: one pass, counts[r] = rows for rank r (host int64[ranks];
+ * synchronous), the rows' destination sets kept in the ctx.  Otherwise (right
+ * after that call, same rows and counts): the rows for rank r, stably compacted, at row
  * sum(counts[<r]) of out (device (capacity, ld_out) f64) with gid_base + index in
  * gid; asynchronous.  The send side of the shard exchange (one all-to-all). */
 int tj_shard_route(tj_ctx* ctx, const double* coords, int64_t n, int64_t ld, int32_t d,

@@ -157,10 +157,13 @@ struct NoStore {
   __device__ void operator()(int64_t, int64_t) const {}
 };
 
-// Points of this rank's rows needed by each of G ranks (owned bins + halo).
+// Points of this rank's rows needed by each of G <= 64 ranks (owned bins + halo):
+// the destination set of every row (a bit mask, kept for the write pass) and the
+// count per destination.
 __global__ void route_count_kernel(const double* __restrict__ x, int64_t n, int64_t ld, Bins b,
                                    const long long* __restrict__ lo, const long long* __restrict__ hi,
-                                   int G, unsigned long long* __restrict__ counts) {
+                                   int G, unsigned long long* __restrict__ counts,
+                                   unsigned long long* __restrict__ dest) {
   extern __shared__ unsigned int s_cnt[];
   for (int r = threadIdx.x; r < G; r += blockDim.x) s_cnt[r] = 0;
   __syncthreads();
@@ -168,13 +171,43 @@ __global__ void route_count_kernel(const double* __restrict__ x, int64_t n, int6
        i += int64_t(gridDim.x) * blockDim.x) {
     long long b0, b1;
     point_bins(x + i * ld, b, b0, b1);
+    unsigned long long m = 0;
     for (int r = 0; r < G; ++r)
-      if (bin_needed(b0, b1, b, lo[r], hi[r])) atomicAdd(&s_cnt[r], 1u);
+      if (bin_needed(b0, b1, b, lo[r], hi[r])) {
+        m |= 1ull << r;
+        atomicAdd(&s_cnt[r], 1u);
+      }
+    dest[i] = m;
   }
   __syncthreads();
   for (int r = threadIdx.x; r < G; r += blockDim.x)
     if (s_cnt[r]) atomicAdd(&counts[r], (unsigned long long)s_cnt[r]);
 }
+
+struct DestCount {
+  const unsigned long long* dest;
+  int r;
+  __device__ int64_t operator()(int64_t i) const { return (dest[i] >> r) & 1ull; }
+};
+
+struct DestWrite {
+  const unsigned long long* dest;
+  int r;
+  const double* x;
+  int64_t ld;
+  int d;
+  double* out;
+  int64_t ld_out;
+  uint32_t* gid;
+  int64_t gid_base;
+  __device__ void operator()(int64_t i, int64_t at) const {
+    if (!((dest[i] >> r) & 1ull)) return;
+    const double* src = x + i * ld;
+    double* dst = out + at * ld_out;
+    for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
+    gid[at] = uint32_t(gid_base + i);
+  }
+};
 
 // First cell c of the local grid whose bin index is >= target (cells are
 // lexicographic, so their prefix bins are non-decreasing).
@@ -297,6 +330,7 @@ void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int
                  int G, int64_t* counts, double* out, int64_t ld_out, uint32_t* gid,
                  int64_t gid_base, int64_t capacity, cudaStream_t s) {
   const Bins b = make_bins(pdims, eps, origin, span);
+  if (G > 64) fail(TJ_EINVAL, "shard_route supports up to 64 ranks");
   if (!out) {  // counts only: one pass over the rows, one read-back
     ctx->tmp64.ensure(sizeof(long long) * (2 * G) + sizeof(unsigned long long) * G + 64, s);
     long long* dlo = reinterpret_cast<long long*>(ctx->tmp64.ptr);
@@ -309,9 +343,10 @@ void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int
     }
     TJ_CUDA(cudaMemcpyAsync(dlo, hlh.data(), sizeof(long long) * 2 * G, cudaMemcpyHostToDevice, s));
     TJ_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * G, s));
+    ctx->route_dest.ensure(sizeof(unsigned long long) * std::max<int64_t>(n, 1), s);
     if (n > 0) {
-      route_count_kernel<<<grid_for(n, 256), 256, sizeof(unsigned) * G, s>>>(x, n, ld, b, dlo, dhi,
-                                                                            G, dcnt);
+      route_count_kernel<<<grid_for(n, 256), 256, sizeof(unsigned) * G, s>>>(
+          x, n, ld, b, dlo, dhi, G, dcnt, ctx->route_dest.as<unsigned long long>());
       TJ_CHECK_LAUNCH();
     }
     std::vector<unsigned long long> hc(G);
@@ -320,15 +355,17 @@ void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int
     for (int r = 0; r < G; ++r) counts[r] = int64_t(hc[r]);
     return;
   }
-  // write: destination r's rows at [sum(counts[<r]), ...), stable (no read-back)
+  // write (after the count call on the same rows: its destination masks):
+  // destination r's rows at [sum(counts[<r]), ...), stable, no read-back
+  const unsigned long long* dest = ctx->route_dest.as<unsigned long long>();
   int64_t off = 0;
   for (int r = 0; r < G; ++r) {
     if (off + counts[r] > capacity) fail(TJ_ECAPACITY, "shard_route: output capacity too small");
     if (counts[r] > 0) {
-      const HaloPred pred{x, ld, b, lo[r], hi[r]};
       ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
-      scan_exclusive(HaloCount{pred},
-                     HaloWrite{pred, d, out + off * ld_out, ld_out, gid + off, gid_base}, n, sc, s);
+      scan_exclusive(DestCount{dest, r},
+                     DestWrite{dest, r, x, ld, d, out + off * ld_out, ld_out, gid + off, gid_base},
+                     n, sc, s);
     }
     off += counts[r];
   }
