@@ -146,7 +146,8 @@ void tj_ctx_destroy(tj_ctx* ctx) {
                     &ctx->masks,    &ctx->win_cell, &ctx->cell_mbase, &ctx->dense,
                     &ctx->pos_off,  &ctx->rows_tmp,  &ctx->SFX,      &ctx->ipos,      &ctx->pcell,
                     &ctx->fwd,      &ctx->bt_start,  &ctx->bt,       &ctx->chunk_key,
-                    &ctx->bt_desc,  &ctx->nid,       &ctx->route_dest};
+                    &ctx->bt_desc,  &ctx->nid,       &ctx->route_dest,
+                    &ctx->route_tiles};
   for (DevBuf* b : bufs) b->release(0);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);

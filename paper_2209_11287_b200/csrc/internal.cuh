@@ -131,7 +131,8 @@ struct tj_ctx {
   tj::DevBuf fwd, bt_start, bt, bt_desc;
   // output id map (tj_set_output_ids): neighbour ids written as out_ids[original id]
   const uint32_t* out_ids = nullptr;
-  tj::DevBuf route_dest;  // shard_route: destination mask of each routed row
+  tj::DevBuf route_dest;   // shard_route: destination mask of each routed row
+  tj::DevBuf route_tiles;  // shard_route: per (destination, warp tile) counts -> offsets
   tj::DevBuf nid;
   bool nid_ready = false;
   bool symmetric = true;

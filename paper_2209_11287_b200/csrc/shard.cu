@@ -184,30 +184,60 @@ __global__ void route_count_kernel(const double* __restrict__ x, int64_t n, int6
     if (s_cnt[r]) atomicAdd(&counts[r], (unsigned long long)s_cnt[r]);
 }
 
-struct DestCount {
-  const unsigned long long* dest;
-  int r;
-  __device__ int64_t operator()(int64_t i) const { return (dest[i] >> r) & 1ull; }
-};
+// Warp-tiled stable routing: warp w of the grid owns rows [w * kRouteRows, +kRouteRows).
+// Pass 1 counts, per destination, the rows of every warp tile (dest-major table);
+// one exclusive scan gives every (destination, tile) its first output row, so the
+// send buffer is destination-major and stable; pass 2 writes.
+constexpr int kRouteRows = 512;
 
-struct DestWrite {
-  const unsigned long long* dest;
-  int r;
-  const double* x;
-  int64_t ld;
-  int d;
-  double* out;
-  int64_t ld_out;
-  uint32_t* gid;
-  int64_t gid_base;
-  __device__ void operator()(int64_t i, int64_t at) const {
-    if (!((dest[i] >> r) & 1ull)) return;
-    const double* src = x + i * ld;
-    double* dst = out + at * ld_out;
-    for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
-    gid[at] = uint32_t(gid_base + i);
+__global__ void route_tile_count_kernel(const unsigned long long* __restrict__ dest, int64_t n,
+                                        int G, int64_t n_tiles, int64_t* __restrict__ tile_cnt) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < n_tiles; t += warps) {
+    const int64_t i0 = t * kRouteRows, i1 = min(n, (t + 1) * kRouteRows);
+    for (int r = 0; r < G; ++r) {  // the tile's masks stay in L1 across destinations
+      unsigned c = 0;
+      for (int64_t i = i0 + lane_id(); i < i1; i += 32) c += unsigned((dest[i] >> r) & 1ull);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane_id() == 0) tile_cnt[int64_t(r) * n_tiles + t] = c;
+    }
   }
-};
+}
+
+__global__ void route_tile_write_kernel(const unsigned long long* __restrict__ dest, int64_t n,
+                                        int G, int64_t n_tiles, const int64_t* __restrict__ tile_off,
+                                        const double* __restrict__ x, int64_t ld, int d,
+                                        double* __restrict__ out, int64_t ld_out,
+                                        uint32_t* __restrict__ gid, int64_t gid_base) {
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const unsigned lt = lanemask_lt();
+  for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < n_tiles; t += warps) {
+    const int64_t i0 = t * kRouteRows, i1 = min(n, (t + 1) * kRouteRows);
+    unsigned long long any = 0;  // destinations present in the tile
+    for (int64_t i = i0 + lane_id(); i < i1; i += 32) any |= dest[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+    while (any) {
+      const int r = __ffsll(any) - 1;
+      any &= any - 1ull;
+      int64_t at = tile_off[int64_t(r) * n_tiles + t];
+      for (int64_t base = i0; base < i1; base += 32) {
+        const int64_t i = base + lane_id();
+        const bool hit = i < i1 && ((dest[i] >> r) & 1ull);
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int64_t o = at + __popc(bal & lt);
+          const double* src = x + i * ld;
+          double* dst = out + o * ld_out;
+          for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
+          gid[o] = uint32_t(gid_base + i);
+        }
+        at += __popc(bal);
+      }
+    }
+  }
+}
 
 // First cell c of the local grid whose bin index is >= target (cells are
 // lexicographic, so their prefix bins are non-decreasing).
@@ -358,17 +388,21 @@ void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int
   // write (after the count call on the same rows: its destination masks):
   // destination r's rows at [sum(counts[<r]), ...), stable, no read-back
   const unsigned long long* dest = ctx->route_dest.as<unsigned long long>();
-  int64_t off = 0;
-  for (int r = 0; r < G; ++r) {
-    if (off + counts[r] > capacity) fail(TJ_ECAPACITY, "shard_route: output capacity too small");
-    if (counts[r] > 0) {
-      ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
-      scan_exclusive(DestCount{dest, r},
-                     DestWrite{dest, r, x, ld, d, out + off * ld_out, ld_out, gid + off, gid_base},
-                     n, sc, s);
-    }
-    off += counts[r];
-  }
+  int64_t total = 0;
+  for (int r = 0; r < G; ++r) total += counts[r];
+  if (total > capacity) fail(TJ_ECAPACITY, "shard_route: output capacity too small");
+  if (n == 0 || total == 0) return;
+  const int64_t n_tiles = ceil_div(n, kRouteRows);
+  ctx->route_tiles.ensure(sizeof(int64_t) * (G * n_tiles + 1), s);
+  int64_t* tiles = ctx->route_tiles.as<int64_t>();
+  const unsigned warp_grid = grid_for(n_tiles * 32, 256);
+  route_tile_count_kernel<<<warp_grid, 256, 0, s>>>(dest, n, G, n_tiles, tiles);
+  TJ_CHECK_LAUNCH();
+  ScanScratch sc = scan_scratch(ctx, G * n_tiles, s);
+  scan_exclusive(LoadAt<int64_t>{tiles}, StoreAt<int64_t>{tiles}, G * n_tiles, sc, s);
+  route_tile_write_kernel<<<warp_grid, 256, 0, s>>>(dest, n, G, n_tiles, tiles, x, ld, d, out, ld_out,
+                                                    gid, gid_base);
+  TJ_CHECK_LAUNCH();
 }
 
 void shard_cell_range(tj_ctx* ctx, int pdims, const int64_t* origin, const int64_t* span,
