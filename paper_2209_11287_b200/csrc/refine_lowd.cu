@@ -18,9 +18,11 @@
 //    2-stage per-warp cp.async ring (5 CTAs = 20 warps per SM: the measured
 //    best ring depth / occupancy); a warp-uniform run cursor maps list offsets
 //    to cell-ordered positions;
-//  * hit test: one DSETP per value against the guard band's upper edge; in a
-//    step with hits a second DSETP + ballot against the lower edge, masked with
-//    the first ballot, finds the values inside the band, which (rare) are re-decided out of line by the reference
+//  * hit test: one DSETP + ballot per value against the guard band's upper
+//    edge; the band itself is pre-tested on the integer pipe (the high word of
+//    D between the band edges' high words, IADD + ISETP), so the FP64 pipe runs
+//    only the DMMA and one DSETP per value; the rare steps where a value is that
+//    near the band re-decide its passing values out of line by the reference
 //    direct form;
 //  * output: the tile's two ballots form one 64-bit hit mask.  One lane writes
 //    each step's masks to the warp's window buffer in shared memory (vector
@@ -70,7 +72,7 @@ struct QuerySide {
   double bq[NG];                 // B fragments per group
   double cq[NG][2];              // FOLD: C operand |q|^2 per column
   double thr[NG][2];             // pass iff D <= thr (upper edge of the guard band)
-  double tlo[NG][2];             // D > tlo: inside the band, decided exactly
+  uint32_t hlo[NG][2], hrg[NG][2];  // band pre-test: high word of D in [hlo, hlo + hrg]
 };
 
 // Guard-band pairs of one tile, re-decided by the reference direct form.
@@ -87,8 +89,9 @@ __device__ __noinline__ uint2 recheck_tile(const double* P, int d, double eps_sq
 }
 
 // U consecutive staged blocks k .. k+U-1 against the NG query groups: all
-// U * NG DMMAs are issued before the first compare, then one DSETP + ballot per
-// value; only steps with a passing value look at the guard band.  Lane 0
+// U * NG DMMAs are issued before the first compare, then one DSETP + ballot and
+// the integer band pre-test per value; only steps with a value near the band
+// leave the fast path.  Lane 0
 // writes the blocks' masks to the warp's window buffer (vector stores).
 template <bool FOLD, int NG, int U>
 __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide<NG>& qs,
@@ -111,7 +114,11 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
       dmma_8x8x4(dv[u][g][0], dv[u][g][1], av[u], qs.bq[g], FOLD ? qs.cq[g][0] : cv[u].x,
                  FOLD ? qs.cq[g][1] : cv[u].y);
   unsigned m[U][NG][2];
-  unsigned any = 0u;
+  // band pre-test on the integer pipe: a value inside the guard band has the
+  // high word of a double between the band edges' high words (same-sign edges:
+  // bit patterns are monotone in magnitude), so one IADD + ISETP per value
+  // replaces a second DSETP on the FP64 pipe the DMMAs use
+  bool near = false;
 #pragma unroll
   for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -119,38 +126,32 @@ __device__ __forceinline__ void lowd_blocks(const RefineArgs& a, const QuerySide
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         m[u][g][j] = __ballot_sync(0xffffffffu, dv[u][g][j] <= qs.thr[g][j]);
-        any |= m[u][g][j];
+        near |= uint32_t(__double2hiint(dv[u][g][j])) - qs.hlo[g][j] <= qs.hrg[g][j];
       }
-  if (any) {
-    // passing values above the band's lower edge are decided exactly: one more
-    // DSETP per value, balloted and masked with the pass ballot (keeping the
-    // pass predicates alive instead makes ptxas recompute them: 3 DSETP/value)
+  if (__any_sync(0xffffffffu, near)) {  // rare: re-decide passing values near the band exactly
     unsigned bm[U][NG][2];
-    unsigned band = 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int g = 0; g < NG; ++g)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          bm[u][g][j] = __ballot_sync(0xffffffffu, dv[u][g][j] > qs.tlo[g][j]) & m[u][g][j];
-          band |= bm[u][g][j];
-        }
-    if (band) {  // warp-uniform
+        for (int j = 0; j < 2; ++j)
+          bm[u][g][j] = __ballot_sync(0xffffffffu, uint32_t(__double2hiint(dv[u][g][j])) - qs.hlo[g][j] <=
+                                                       qs.hrg[g][j]) &
+                        m[u][g][j];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          if (bm[u][g][0] | bm[u][g][1]) {
-            const uint2 mm = recheck_tile(a.P, a.d, a.eps_sq, (bm[u][g][0] >> lane) & 1u,
-                                          (bm[u][g][1] >> lane) & 1u, m[u][g][0], m[u][g][1],
-                                          q0 + 8 * g + 2 * col, s->pos[8 * (k + u) + row],
-                                          &a.ctr->rechecks);
-            m[u][g][0] = mm.x;
-            m[u][g][1] = mm.y;
-          }
+      for (int g = 0; g < NG; ++g) {
+        if (bm[u][g][0] | bm[u][g][1]) {
+          const uint2 mm = recheck_tile(a.P, a.d, a.eps_sq, (bm[u][g][0] >> lane) & 1u,
+                                        (bm[u][g][1] >> lane) & 1u, m[u][g][0], m[u][g][1],
+                                        q0 + 8 * g + 2 * col, s->pos[8 * (k + u) + row],
+                                        &a.ctr->rechecks);
+          m[u][g][0] = mm.x;
+          m[u][g][1] = mm.y;
         }
-    }
+      }
   }
   // the block's masks into the window buffer (one lane, vector stores)
   if (lane == 0) {
@@ -201,7 +202,14 @@ __device__ __forceinline__ void lowd_item(const RefineArgs& a, const WorkItem& i
       const double hi = center + guard, lo = center - guard;
       qs.cq[g][j] = qn;
       qs.thr[g][j] = v ? hi : -INFINITY;
-      qs.tlo[g][j] = v ? lo : INFINITY;
+      const uint32_t hh = uint32_t(__double2hiint(hi)), hl = uint32_t(__double2hiint(lo));
+      if ((hh ^ hl) >> 31) {  // edges of opposite signs (band around 0): always re-decide
+        qs.hlo[g][j] = 0u;
+        qs.hrg[g][j] = 0xffffffffu;
+      } else {
+        qs.hlo[g][j] = min(hh, hl);
+        qs.hrg[g][j] = max(hh, hl) - min(hh, hl);
+      }
     }
   }
   const int nst = (nblk + 7) >> 3;
