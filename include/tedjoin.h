@@ -287,6 +287,14 @@ int tj_scatter_counts(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const
 /* offsets[0..n] = exclusive prefix sum of counts[0..n-1] (device).  Async. */
 int tj_counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
                          void* stream);
+/* The same exchange with one byte per id: counts[gid[l]] = min(row length, 255)
+ * and *overflow |= 1 when a row is longer (device int32, zeroed by the caller;
+ * any overflow on any rank -> use the int32 pair above).  The all-reduce of the
+ * counts then moves n bytes instead of 4n.  Async. */
+int tj_scatter_counts_u8(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const uint32_t* gid,
+                         uint8_t* counts, int32_t* overflow, void* stream);
+int tj_counts_u8_to_offsets(tj_ctx* ctx, const uint8_t* counts, int64_t n, int64_t* offsets,
+                            void* stream);
 /* Copy every non-empty local row l (neighbors already global ids) to
  * dst[global_offsets[gid[l]] ...]; dst may be device memory or mapped pinned
  * host memory (cudaHostRegisterMapped), so ranks write one shared host CSR.  Async. */

@@ -85,6 +85,8 @@ SIGNATURES = {
     "tj_remap_ids": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "tj_scatter_counts": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "tj_counts_to_offsets": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "tj_scatter_counts_u8": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "tj_counts_u8_to_offsets": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "tj_place_rows": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "tj_fp64_peak": (_i32, [_i32, _i32, ctypes.POINTER(_f64), ctypes.POINTER(_f64)]),
     "tj_dmma_known_answer": (_i32, [_vp, _vp, _vp, _vp]),
@@ -376,14 +378,26 @@ class Context:
         self._check(self.lib.tj_remap_ids(self.handle, ids.data_ptr() if m else None, int(m),
                                           gid.data_ptr(), self.stream().cuda_stream))
 
-    def scatter_counts(self, offsets, n_rows: int, gid, counts):
-        self._check(self.lib.tj_scatter_counts(self.handle, offsets.data_ptr(), int(n_rows),
-                                               gid.data_ptr(), counts.data_ptr(),
-                                               self.stream().cuda_stream))
+    def scatter_counts(self, offsets, n_rows: int, gid, counts, overflow=None):
+        """counts (int32, or uint8 with an int32 `overflow` flag) [gid[l]] = row l's length."""
+        import torch
+
+        if counts.dtype == torch.uint8:
+            self._check(self.lib.tj_scatter_counts_u8(self.handle, offsets.data_ptr(), int(n_rows),
+                                                      gid.data_ptr(), counts.data_ptr(),
+                                                      overflow.data_ptr(), self.stream().cuda_stream))
+        else:
+            self._check(self.lib.tj_scatter_counts(self.handle, offsets.data_ptr(), int(n_rows),
+                                                   gid.data_ptr(), counts.data_ptr(),
+                                                   self.stream().cuda_stream))
 
     def counts_to_offsets(self, counts, n: int, offsets):
-        self._check(self.lib.tj_counts_to_offsets(self.handle, counts.data_ptr(), int(n),
-                                                  offsets.data_ptr(), self.stream().cuda_stream))
+        import torch
+
+        fn = (self.lib.tj_counts_u8_to_offsets if counts.dtype == torch.uint8
+              else self.lib.tj_counts_to_offsets)
+        self._check(fn(self.handle, counts.data_ptr(), int(n), offsets.data_ptr(),
+                       self.stream().cuda_stream))
 
     def place_rows(self, offsets, neighbors, n_rows: int, gid, global_offsets, dst_ptr: int):
         self._check(self.lib.tj_place_rows(self.handle, offsets.data_ptr(), neighbors.data_ptr(),

@@ -880,6 +880,22 @@ int tj_scatter_counts(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const
   });
 }
 
+int tj_scatter_counts_u8(tj_ctx* ctx, const int64_t* offsets, int64_t n_rows, const uint32_t* gid,
+                         uint8_t* counts, int32_t* overflow, void* stream) {
+  if (!ctx || !overflow || (n_rows > 0 && (!offsets || !gid || !counts))) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    shard_scatter_counts_u8(offsets, n_rows, gid, counts, overflow, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tj_counts_u8_to_offsets(tj_ctx* ctx, const uint8_t* counts, int64_t n, int64_t* offsets,
+                            void* stream) {
+  if (!ctx || !offsets || (n > 0 && !counts) || n < 0) return TJ_EINVAL;
+  return guarded(ctx, [&] {
+    counts_to_offsets_u8(ctx, counts, n, offsets, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int tj_counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
                          void* stream) {
   if (!ctx || !offsets || (n > 0 && !counts) || n < 0) return TJ_EINVAL;

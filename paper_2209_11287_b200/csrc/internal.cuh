@@ -222,6 +222,10 @@ void shard_place_rows(const int64_t* loff, const uint32_t* nbr, int64_t n_rows, 
                       const int64_t* goff, uint32_t* dst, cudaStream_t s);
 void counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
                        cudaStream_t s);
+void shard_scatter_counts_u8(const int64_t* loff, int64_t n_rows, const uint32_t* gid,
+                             uint8_t* counts, int32_t* overflow, cudaStream_t s);
+void counts_to_offsets_u8(tj_ctx* ctx, const uint8_t* counts, int64_t n, int64_t* offsets,
+                          cudaStream_t s);
 void launch_count_rows(tj_ctx* ctx, int64_t cb, int64_t ce, unsigned long long* hits,
                        unsigned long long* max_row, cudaStream_t s);
 void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* neighbors, int64_t n_pairs,

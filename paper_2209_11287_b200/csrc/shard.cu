@@ -274,6 +274,22 @@ __global__ void scatter_counts_kernel(const int64_t* __restrict__ loff, int64_t 
   }
 }
 
+// One byte per id when every row is shorter than 256 (the usual case: the
+// all-reduce then moves n bytes instead of 4n); longer rows set *overflow and
+// the caller falls back to the int32 counts.
+__global__ void scatter_counts_u8_kernel(const int64_t* __restrict__ loff, int64_t n_rows,
+                                         const uint32_t* __restrict__ gid,
+                                         uint8_t* __restrict__ counts, int32_t* overflow) {
+  bool over = false;
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < n_rows;
+       l += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = loff[l + 1] - loff[l];
+    if (c) counts[gid[l]] = uint8_t(c > 255 ? 255 : c);
+    over |= c > 255;
+  }
+  if (__any_sync(0xffffffffu, over) && lane_id() == 0) atomicOr(overflow, 1);
+}
+
 // Warp per local row: copy the row (ids already global) to its global offset.
 __global__ void place_rows_kernel(const int64_t* __restrict__ loff, const uint32_t* __restrict__ nbr,
                                   int64_t n_rows, const uint32_t* __restrict__ gid,
@@ -434,6 +450,13 @@ void shard_scatter_counts(const int64_t* loff, int64_t n_rows, const uint32_t* g
   TJ_CHECK_LAUNCH();
 }
 
+void shard_scatter_counts_u8(const int64_t* loff, int64_t n_rows, const uint32_t* gid,
+                             uint8_t* counts, int32_t* overflow, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  scatter_counts_u8_kernel<<<grid_for(n_rows, 256), 256, 0, s>>>(loff, n_rows, gid, counts, overflow);
+  TJ_CHECK_LAUNCH();
+}
+
 void shard_place_rows(const int64_t* loff, const uint32_t* nbr, int64_t n_rows, const uint32_t* gid,
                       const int64_t* goff, uint32_t* dst, cudaStream_t s) {
   if (n_rows <= 0) return;
@@ -441,11 +464,22 @@ void shard_place_rows(const int64_t* loff, const uint32_t* nbr, int64_t n_rows, 
   TJ_CHECK_LAUNCH();
 }
 
+template <class T>
+static void counts_to_offsets_t(tj_ctx* ctx, const T* counts, int64_t n, int64_t* offsets,
+                                cudaStream_t s) {
+  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
+  scan_exclusive(LoadAt<T>{counts}, StoreAt<int64_t>{offsets}, n, sc, s);
+  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+}
+
 void counts_to_offsets(tj_ctx* ctx, const int32_t* counts, int64_t n, int64_t* offsets,
                        cudaStream_t s) {
-  ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(n, 1), s);
-  scan_exclusive(LoadAt<int32_t>{counts}, StoreAt<int64_t>{offsets}, n, sc, s);
-  TJ_CUDA(cudaMemcpyAsync(offsets + n, sc.total, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  counts_to_offsets_t(ctx, counts, n, offsets, s);
+}
+
+void counts_to_offsets_u8(tj_ctx* ctx, const uint8_t* counts, int64_t n, int64_t* offsets,
+                          cudaStream_t s) {
+  counts_to_offsets_t(ctx, counts, n, offsets, s);
 }
 
 }  // namespace tj

@@ -21,7 +21,8 @@ batch's cells (join.py:184-197) -- with the strong layout of SURVEY.md 8(e):
    ids (tj_set_output_ids: local ids are monotone in global ids, so rows stay
    sorted);
 6. global row offsets: each rank scatters its row counts to global ids
-   (tj_scatter_counts), one SUM all-reduce of n int32 counts, one scan.
+   (tj_scatter_counts_u8), one SUM all-reduce of n one-byte counts (int32 when
+   a row reaches 256 ids), one scan.
 The pair set then sits on the devices, each rank holding its rows and every
 rank the global offsets: no O(|R|) buffer exists on any rank.  To land it on
 the host, every rank writes its rows straight to their final places in one
@@ -262,6 +263,37 @@ def row_slice(n: int, rank: int, world: int) -> tuple[int, int]:
     return min(n, rank * per), min(n, (rank + 1) * per)
 
 
+def exchange_counts(ctx, loff, n_local: int, gid, n: int, dev, group=None):
+    """Global per-id row counts: every rank scatters its rows' lengths to their
+    global ids and the ranks SUM-all-reduce the n counts (each id is owned by one
+    rank).  One byte per id while every row is shorter than 256 (a 4-byte MAX
+    all-reduce of the overflow flag decides), else int32."""
+    import torch
+    import torch.distributed as dist
+
+    gloo = dist.get_backend(group) == "gloo"
+
+    def reduce(t, op):
+        if gloo:  # gloo reduces host tensors
+            c = t.cpu()
+            _all_reduce(c, op, group)
+            return c.to(dev)
+        _all_reduce(t, op, group)
+        return t
+
+    c8 = torch.zeros(n, dtype=torch.uint8, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    if n_local:
+        ctx.scatter_counts(loff, n_local, gid, c8, ovf)
+    if int(reduce(ovf, dist.ReduceOp.MAX).item()) == 0:
+        return reduce(c8, dist.ReduceOp.SUM)
+    del c8
+    counts = torch.zeros(n, dtype=torch.int32, device=dev)
+    if n_local:
+        ctx.scatter_counts(loff, n_local, gid, counts)
+    return reduce(counts, dist.ReduceOp.SUM)
+
+
 def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> ShardResult:
     """The strong layout's join step over the process group (steps 2-6 above).
 
@@ -307,15 +339,7 @@ def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> Sh
         lnbr = torch.empty(1, dtype=torch.int32, device=dev)
         mark("index")
         mark("refine")
-    counts = torch.zeros(n, dtype=torch.int32, device=dev)
-    if n_local:
-        ctx.scatter_counts(loff, n_local, gid, counts)
-    if dist.get_backend(group) == "gloo":
-        c = counts.cpu()
-        _all_reduce(c, dist.ReduceOp.SUM, group)
-        counts = c.to(dev)
-    else:
-        _all_reduce(counts, dist.ReduceOp.SUM, group)
+    counts = exchange_counts(ctx, loff, n_local, gid, n, dev, group)
     goff = torch.empty(n + 1, dtype=torch.int64, device=dev)
     ctx.counts_to_offsets(counts, n, goff)
     mark("offsets")

@@ -128,10 +128,15 @@ def _strong_worker(rank, world, port, eps, shm_path, out_q):
         assert np.all(np.diff(owned) == 1) or len(owned) <= 1  # one contiguous cell range
         loff, lnb = oracle.join_csr(local, eps, cells=owned)
         gnb = gid[lnb.astype(np.int64)]
-        counts = torch.zeros(n, dtype=torch.int64)
-        counts[gid] = torch.from_numpy(np.diff(loff))
+        # global offsets as distributed.exchange_counts: one byte per id unless a
+        # row reaches 256 ids on some rank (MAX all-reduce of the flag), else int32
+        lens = np.diff(loff)
+        ovf = torch.tensor([int(np.any(lens > 255))], dtype=torch.int32)
+        dist.all_reduce(ovf, op=dist.ReduceOp.MAX)
+        counts = torch.zeros(n, dtype=torch.uint8 if int(ovf) == 0 else torch.int32)
+        counts[gid] = torch.from_numpy(np.minimum(lens, 255) if int(ovf) == 0 else lens).to(counts.dtype)
         dist.all_reduce(counts, op=dist.ReduceOp.SUM)
-        goff = np.concatenate([[0], np.cumsum(counts.numpy())])
+        goff = np.concatenate([[0], np.cumsum(counts.numpy().astype(np.int64))])
         if rank == 0:
             np.zeros(int(goff[-1]), np.int64).tofile(shm_path)
         dist.barrier()

@@ -98,8 +98,12 @@ def rank_step(plan, r, G):
     t.append(ev())
     ctx.set_output_ids(gid)
     loff, lnbr = job.finalize()
-    counts = torch.zeros(n, dtype=torch.int32, device=dev)
-    ctx.scatter_counts(loff, n_local, gid, counts)
+    counts = torch.zeros(n, dtype=torch.uint8, device=dev)  # distributed.exchange_counts
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctx.scatter_counts(loff, n_local, gid, counts, ovf)
+    if int(ovf.item()):
+        counts = torch.zeros(n, dtype=torch.int32, device=dev)
+        ctx.scatter_counts(loff, n_local, gid, counts)
     goff = torch.empty(n + 1, dtype=torch.int64, device=dev)
     ctx.counts_to_offsets(counts, n, goff)
     t.append(ev())
@@ -107,7 +111,7 @@ def rank_step(plan, r, G):
     ph = [t[i].elapsed_time(t[i + 1]) for i in range(5)]
     return {"rank": r, "n_local": n_local, "pairs": pairs, "route_ms": ph[0], "index_ms": ph[2],
             "refine_ms": ph[3], "output_ms": ph[4], "step_ms": ph[0] + ph[2] + ph[3] + ph[4],
-            "recv_bytes": n_local * (coords.shape[1] * 8 + 4)}
+            "recv_bytes": n_local * (coords.shape[1] * 8 + 4), "count_bytes": counts.element_size()}
 
 
 out = {"config": name, "n": n, "d": d, "T1_ms": T1, "nvlink_bus_gbs_assumed": NVLINK_BUS_GBS,
@@ -120,7 +124,7 @@ for G in Gs:
     ranks = [rank_step(plan, r, G) for r in range(G)]  # second pass: warm allocator
     worst = max(ranks, key=lambda x: x["step_ms"])
     coll_bytes = {"all_to_all_points": (G - 1) / G * worst["recv_bytes"],
-                  "all_reduce_counts": 2 * (G - 1) / G * n * 4}
+                  "all_reduce_counts": 2 * (G - 1) / G * n * max(x["count_bytes"] for x in ranks)}
     coll_ms = sum(b / (NVLINK_BUS_GBS * 1e9) * 1e3 for b in coll_bytes.values())
     TG = worst["step_ms"] + coll_ms
     row = {"G": G, "slowest_rank": worst, "mean_rank_ms": float(np.mean([x["step_ms"] for x in ranks])),
