@@ -211,7 +211,7 @@ def test_halo_mask_matches_definition():
                 assert got[i] == want
 
 
-def _gpu_worker(rank, world, port, eps, kernel, out_q):
+def _gpu_worker(rank, world, port, case, kernel, out_q):
     """The real strong layout (strong_self_join: bin plan, all-gather, tj_shard_select,
     tj_refine of the owned cells, global offsets, rows placed in the shared mapped host
     CSR) with two ranks sharing cuda:0 over gloo (NCCL needs distinct GPUs)."""
@@ -226,7 +226,8 @@ def _gpu_worker(rank, world, port, eps, kernel, out_q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ds = generate(GenSpec("uniform", 40_000, 4, seed=4)) if rank == 0 else None
+        dist_, n, d, eps = case
+        ds = generate(GenSpec(dist_, n, d, seed=4)) if rank == 0 else None
         shard, merged = shard_self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, device=0))
         info = (shard.pairs, shard.n_local, shard.total_pairs)
         if rank == 0:
@@ -237,14 +238,20 @@ def _gpu_worker(rank, world, port, eps, kernel, out_q):
         dist.destroy_process_group()
 
 
+# (uniform 4-D: one-byte count exchange; uniform 2-D at ~250 neighbours per point:
+#  rows of 256+ ids force the int32 fallback of distributed.exchange_counts)
+GPU_CASES = [("uniform", 40_000, 4, 0.06), ("uniform", 8_000, 2, 0.1)]
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", GPU_CASES)
 @pytest.mark.parametrize("kernel", ["tile", "scalar"])
-def test_two_rank_shard_self_join_on_gpu(kernel):
-    world, eps = 2, 0.06
+def test_two_rank_shard_self_join_on_gpu(kernel, case):
+    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, eps, kernel, q))
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, case, kernel, q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -252,8 +259,11 @@ def test_two_rank_shard_self_join_on_gpu(kernel):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ds = generate(GenSpec("uniform", 40_000, 4, seed=4))
+    dist_, n, d, eps = case
+    ds = generate(GenSpec(dist_, n, d, seed=4))
     full_off, full_nb = oracle.join_csr(ds, eps)
+    if d == 2:
+        assert np.diff(full_off).max() > 255  # the int32 count exchange runs
     merged = [r for r in results if r[0] is not None][0]
     assert np.array_equal(merged[0], full_off)
     assert np.array_equal(np.asarray(merged[1], np.int64), full_nb.astype(np.int64))
