@@ -116,8 +116,10 @@ __global__ void cell_minmax_kernel(const double* __restrict__ x, int64_t n, int 
   }
 }
 
+// K = uint32_t when the packed key has <= 32 bits (the radix sort moves 4 bytes less per key).
+template <class K>
 __global__ void cell_key_kernel(const double* __restrict__ x, int64_t n, int ld, double eps,
-                                KeyParams kp, uint64_t* __restrict__ keys) {
+                                KeyParams kp, K* __restrict__ keys) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     uint64_t key = 0;
@@ -128,12 +130,15 @@ __global__ void cell_key_kernel(const double* __restrict__ x, int64_t n, int ld,
         key |= uint64_t(c - kp.cmin[j] + 1) << kp.shift[j];
       }
     }
-    keys[i] = key;
+    keys[i] = K(key);
   }
 }
 
 // Cell-ordered zero-padded coordinates, chunk norms in the reference order
 // ((((0+x0^2)+x1^2)+x2^2)+x3^2 per chunk, kernels.py:126-130) and full norms.
+// One chunk (d <= 4): the chunk norm is the norm, CN is not written (only the
+// d > 4 kernels read it).  Rows are read as double2 when the row stride is even.
+template <bool VEC>
 __global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, int d, int d_pad,
                                const uint32_t* __restrict__ perm, double* __restrict__ P,
                                double* __restrict__ CN, double* __restrict__ NRM,
@@ -148,24 +153,33 @@ __global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, 
     double total = 0.0;
     for (int c = 0; c < nchunks; ++c) {
       double v[4];
+      if (VEC && 4 * c + 4 <= d) {
+        const double2 lo = __ldg(reinterpret_cast<const double2*>(src + 4 * c));
+        const double2 hi = __ldg(reinterpret_cast<const double2*>(src + 4 * c + 2));
+        v[0] = lo.x;
+        v[1] = lo.y;
+        v[2] = hi.x;
+        v[3] = hi.y;
+      } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int j = 4 * c + t;
-        v[t] = j < d ? src[j] : 0.0;
+        for (int t = 0; t < 4; ++t) {
+          const int j = 4 * c + t;
+          v[t] = j < d ? __ldg(src + j) : 0.0;
+        }
       }
-      double2* dst2 = reinterpret_cast<double2*>(dst + 4 * c);
-      dst2[0] = make_double2(v[0], v[1]);
-      dst2[1] = make_double2(v[2], v[3]);
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) s = __dadd_rn(s, __dmul_rn(v[t], v[t]));
-      CN[p * nchunks + c] = s;
+      // d <= 3: the padding coordinate carries |x|^2 for the norm-in-K DMMA tile
+      // (refine_lowd.cu); every reader of P uses only the first d coordinates otherwise.
+      if (nchunks == 1 && d <= 3) v[3] = s;
+      double2* dst2 = reinterpret_cast<double2*>(dst + 4 * c);
+      dst2[0] = make_double2(v[0], v[1]);
+      dst2[1] = make_double2(v[2], v[3]);
+      if (nchunks > 1) CN[p * nchunks + c] = s;
       total = __dadd_rn(total, s);
     }
     NRM[p] = total;
-    // d <= 3: the padding coordinate carries |x|^2 for the norm-in-K DMMA tile
-    // (refine_lowd.cu); every reader of P uses only the first d coordinates otherwise.
-    if (d <= 3) dst[3] = total;
     local_max = max(local_max, (unsigned long long)__double_as_longlong(total));
   }
   for (int o = 16; o > 0; o >>= 1)
@@ -187,17 +201,19 @@ __global__ void suffix_kernel(const double* __restrict__ CN, const double* __res
   }
 }
 
+template <class K>
 struct HeadFlag {
-  const uint64_t* keys;
+  const K* keys;
   __device__ int64_t operator()(int64_t i) const { return i == 0 || keys[i] != keys[i - 1]; }
 };
+template <class K>
 struct CellTableOut {
-  const uint64_t* keys;
+  const K* keys;
   uint64_t* cell_key;
   int64_t* cell_start;
   __device__ void operator()(int64_t i, int64_t excl) const {
     if (i == 0 || keys[i] != keys[i - 1]) {
-      cell_key[excl] = keys[i];
+      cell_key[excl] = uint64_t(keys[i]);
       cell_start[excl] = i;
     }
   }
@@ -278,12 +294,75 @@ __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key,
   e = cell_start[z];
 }
 
+// Dense lookup of U cells at once (lane = neighbour row): the three box entries
+// of every cell's row, then their position ranges -- U independent load chains
+// per lane instead of one (the kernels below are load-latency bound).
+template <int U>
+__device__ __forceinline__ void dense_rows(const RowParams& rp, const uint64_t (&key)[U], int r,
+                                           const int64_t* __restrict__ cell_start,
+                                           int64_t (&b)[U], int64_t (&e)[U]) {
+  long long delta = 0;
+  int rr = r;
+  for (int j = rp.k - 2; j >= 0; --j) {
+    delta += (long long)(rr % 3 - 1) * rp.dstride[j];
+    rr /= 3;
+  }
+  int cc[U][3];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long idx = dense_index(rp, key[u]) + delta;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) cc[u][t] = __ldg(rp.dense + idx - 1 + t);
+  }
+  int64_t sb[U], se[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int first = cc[u][0] >= 0 ? cc[u][0] : (cc[u][1] >= 0 ? cc[u][1] : cc[u][2]);
+    const int last = cc[u][2] >= 0 ? cc[u][2] : (cc[u][1] >= 0 ? cc[u][1] : cc[u][0]);
+    sb[u] = first >= 0 ? __ldg(cell_start + first) : 0;
+    se[u] = first >= 0 ? __ldg(cell_start + last + 1) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    b[u] = sb[u];
+    e[u] = se[u];
+  }
+}
+
+constexpr int kCandU = 4;  // cells per warp iteration (dense lookup)
+
 // Warp per cell: number of non-empty runs and candidates.
 __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
                                   const int64_t* __restrict__ cell_start, int64_t n_cells,
                                   int64_t* __restrict__ run_count, int64_t* __restrict__ cand_count) {
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
+  const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (rp.dense && rp.n_rows <= 32) {
+    const int r = lane_id();
+    for (int64_t c0 = w0 * kCandU; c0 < n_cells; c0 += warps * kCandU) {
+      uint64_t key[kCandU];
+#pragma unroll
+      for (int u = 0; u < kCandU; ++u) key[u] = c0 + u < n_cells ? cell_key[c0 + u] : cell_key[c0];
+      int64_t b[kCandU], e[kCandU];
+      if (r < rp.n_rows) {
+        dense_rows<kCandU>(rp, key, r, cell_start, b, e);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kCandU; ++u) b[u] = e[u] = 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCandU; ++u) {
+        const int64_t runs = __popc(__ballot_sync(0xffffffffu, e[u] > b[u]));
+        const int64_t cands = warp_sum(e[u] - b[u]);
+        if (lane_id() == 0 && c0 + u < n_cells) {
+          run_count[c0 + u] = runs;
+          cand_count[c0 + u] = cands;
+        }
+      }
+    }
+    return;
+  }
+  for (int64_t c = w0; c < n_cells; c += warps) {
     const uint64_t key = cell_key[c];
     int64_t runs = 0, cands = 0;
     for (int r = lane_id(); r < rp.n_rows; r += 32) {
@@ -309,7 +388,38 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
                                  uint32_t* __restrict__ run_off) {
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const unsigned lt = lanemask_lt();
-  for (int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; c < n_cells; c += warps) {
+  const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (rp.dense && rp.n_rows <= 32) {
+    const int r = lane_id();
+    for (int64_t c0 = w0 * kCandU; c0 < n_cells; c0 += warps * kCandU) {
+      uint64_t key[kCandU];
+      int64_t out[kCandU];
+#pragma unroll
+      for (int u = 0; u < kCandU; ++u) {
+        key[u] = c0 + u < n_cells ? cell_key[c0 + u] : cell_key[c0];
+        out[u] = c0 + u < n_cells ? cell_runs[c0 + u] : 0;
+      }
+      int64_t b[kCandU], e[kCandU];
+      if (r < rp.n_rows) {
+        dense_rows<kCandU>(rp, key, r, cell_start, b, e);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kCandU; ++u) b[u] = e[u] = 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCandU; ++u) {
+        const unsigned m = __ballot_sync(0xffffffffu, e[u] > b[u]);
+        const int64_t len = e[u] - b[u];
+        const int64_t inc = warp_inclusive_scan(len);
+        if (e[u] > b[u] && c0 + u < n_cells) {
+          runs[out[u] + __popc(m & lt)] = make_uint2(uint32_t(b[u]), uint32_t(e[u]));
+          run_off[out[u] + __popc(m & lt)] = uint32_t(inc - len);
+        }
+      }
+    }
+    return;
+  }
+  for (int64_t c = w0; c < n_cells; c += warps) {
     const uint64_t key = cell_key[c];
     int64_t out = cell_runs[c];
     int64_t off = 0;  // offset of the next run inside the concatenated candidate list
@@ -439,35 +549,58 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
     kp.shift[j] = g.shift[j];
     kp.cmin[j] = g.cmin[j];
   }
-  cell_key_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, ctx->keys.as<uint64_t>());
-  TJ_CHECK_LAUNCH();
   const int64_t hist_elems = radix_sort_scratch_elems(n);
   ctx->sort_hist.ensure(sizeof(int64_t) * hist_elems, s);
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
-  int where = radix_sort_pairs(ctx->keys.as<uint64_t>(), ctx->perm.as<uint32_t>(),
-                               ctx->keys_alt.as<uint64_t>(), ctx->vals_alt.as<uint32_t>(), n,
-                               total_bits, true, ctx->sort_hist.as<int64_t>(), sc, s);
-  if (where == 1) {
-    std::swap(ctx->keys, ctx->keys_alt);
-    std::swap(ctx->perm, ctx->vals_alt);
-  }
-  const uint64_t* keys = ctx->keys.as<uint64_t>();
-
-  // 4. run table of non-empty cells
   ctx->cell_key.ensure(sizeof(uint64_t) * (n + 1), s);
   ctx->cell_start.ensure(sizeof(int64_t) * (n + 1), s);
-  scan_exclusive(HeadFlag{keys},
-                 CellTableOut{keys, ctx->cell_key.as<uint64_t>(), ctx->cell_start.as<int64_t>()},
-                 n, sc, s);
+  if (total_bits <= 32) {
+    uint32_t* k0 = ctx->keys.as<uint32_t>();
+    uint32_t* k1 = ctx->keys_alt.as<uint32_t>();
+    cell_key_kernel<uint32_t><<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, k0);
+    TJ_CHECK_LAUNCH();
+    const int where = radix_sort_pairs32(k0, ctx->perm.as<uint32_t>(), k1,
+                                         ctx->vals_alt.as<uint32_t>(), n, total_bits, true,
+                                         ctx->sort_hist.as<int64_t>(), sc, s);
+    if (where == 1) {
+      std::swap(ctx->keys, ctx->keys_alt);
+      std::swap(ctx->perm, ctx->vals_alt);
+    }
+    // 4. run table of non-empty cells
+    const uint32_t* keys = ctx->keys.as<uint32_t>();
+    scan_exclusive(HeadFlag<uint32_t>{keys},
+                   CellTableOut<uint32_t>{keys, ctx->cell_key.as<uint64_t>(),
+                                          ctx->cell_start.as<int64_t>()},
+                   n, sc, s);
+  } else {
+    uint64_t* k0 = ctx->keys.as<uint64_t>();
+    uint64_t* k1 = ctx->keys_alt.as<uint64_t>();
+    cell_key_kernel<uint64_t><<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, k0);
+    TJ_CHECK_LAUNCH();
+    const int where = radix_sort_pairs(k0, ctx->perm.as<uint32_t>(), k1,
+                                       ctx->vals_alt.as<uint32_t>(), n, total_bits, true,
+                                       ctx->sort_hist.as<int64_t>(), sc, s);
+    if (where == 1) {
+      std::swap(ctx->keys, ctx->keys_alt);
+      std::swap(ctx->perm, ctx->vals_alt);
+    }
+    const uint64_t* keys = ctx->keys.as<uint64_t>();
+    scan_exclusive(HeadFlag<uint64_t>{keys},
+                   CellTableOut<uint64_t>{keys, ctx->cell_key.as<uint64_t>(),
+                                          ctx->cell_start.as<int64_t>()},
+                   n, sc, s);
+  }
   g.n_cells = read_scalar<int64_t>(sc.total, s);
   TJ_CUDA(cudaMemcpyAsync(ctx->cell_start.as<int64_t>() + g.n_cells, &n, sizeof(int64_t),
                           cudaMemcpyHostToDevice, s));
 
   // 5. cell-ordered coordinates + norms
   ctx->P.ensure(sizeof(double) * n * g.d_pad, s);
-  ctx->CN.ensure(sizeof(double) * n * g.nchunks, s);
+  if (g.nchunks > 1) ctx->CN.ensure(sizeof(double) * n * g.nchunks, s);
   ctx->NRM.ensure(sizeof(double) * n, s);
-  permute_kernel<<<grid_for(n, 256), 256, 0, s>>>(
+  const bool vec = ld % 2 == 0 && d >= 4 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  auto permute = vec ? permute_kernel<true> : permute_kernel<false>;
+  permute<<<grid_for(n, 256), 256, 0, s>>>(
       x, n, ld, d, g.d_pad, ctx->perm.as<uint32_t>(), ctx->P.as<double>(), ctx->CN.as<double>(),
       ctx->NRM.as<double>(), reinterpret_cast<unsigned long long*>(mm + 2 * TJ_MAX_K_IDX));
   TJ_CHECK_LAUNCH();
@@ -512,7 +645,7 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   ctx->cell_cand.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->cell_cost.ensure(sizeof(int64_t) * (nc + 1), s);
   ctx->tmp64.ensure(sizeof(int64_t) * (nc + 1), s);
-  const unsigned warp_blocks = grid_for(nc * 32, 256);
+  const unsigned warp_blocks = grid_for(ceil_div(nc, rp.dense ? kCandU : 1) * 32, 256);
   cand_count_kernel<<<warp_blocks, 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
                                                 ctx->cell_start.as<int64_t>(), nc,
                                                 ctx->tmp64.as<int64_t>(),

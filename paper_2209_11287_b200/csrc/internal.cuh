@@ -161,6 +161,9 @@ int64_t radix_sort_scratch_elems(int64_t n);
 int radix_sort_pairs(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, int64_t n,
                      int key_bits, bool identity_values, int64_t* hist, ScanScratch scan,
                      cudaStream_t stream);
+int radix_sort_pairs32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n,
+                       int key_bits, bool identity_values, int64_t* hist, ScanScratch scan,
+                       cudaStream_t stream);
 // grid.cu
 void build_grid(tj_ctx* ctx, const double* coords, int64_t n, int d, int64_t ld, int k,
                 double eps, cudaStream_t s);
