@@ -139,7 +139,7 @@ void tj_ctx_destroy(tj_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&ctx->P,        &ctx->NRM,       &ctx->CN,       &ctx->perm,      &ctx->keys,
-                    &ctx->cell_key, &ctx->cell_start, &ctx->cell_runs, &ctx->runs,      &ctx->run_off,
+                    &ctx->cell_key, &ctx->cell_key_hi, &ctx->keys_hi, &ctx->cell_start, &ctx->cell_runs, &ctx->runs,      &ctx->run_off,
                     &ctx->cell_cand, &ctx->cell_cost, &ctx->keys_alt,  &ctx->vals_alt,  &ctx->sort_hist,
                     &ctx->scan_partial, &ctx->scan_total, &ctx->minmax, &ctx->tmp64,   &ctx->items,
                     &ctx->pairs,    &ctx->qcount,    &ctx->counters, &ctx->fill,
@@ -211,16 +211,21 @@ int tj_get_grid_info(tj_ctx* ctx, tj_grid_info* out) {
   });
 }
 
-// Decode packed cell keys back into cell coordinates.
-__global__ void decode_keys_kernel(const uint64_t* keys, int64_t n_cells, int k,
-                                   const int* shift, const long long* cmin, int64_t* out) {
+// Decode packed cell keys (one or two words) back into cell coordinates.
+struct KeyLayout {
+  int k;
+  int shift[TJ_MAX_K_IDX], bits[TJ_MAX_K_IDX], word[TJ_MAX_K_IDX];
+  long long cmin[TJ_MAX_K_IDX];
+};
+__global__ void decode_keys_kernel(const uint64_t* keys, const uint64_t* keys_hi, int64_t n_cells,
+                                   KeyLayout L, int64_t* out) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
        c += int64_t(gridDim.x) * blockDim.x) {
-    for (int j = 0; j < k; ++j) {
-      const int hi = j == 0 ? 64 : shift[j - 1];
-      const int bits = hi - shift[j];
-      const uint64_t f = (keys[c] >> shift[j]) & (bits >= 64 ? ~0ull : ((1ull << bits) - 1));
-      out[c * k + j] = int64_t(f) - 1 + cmin[j];
+    for (int j = 0; j < L.k; ++j) {
+      const uint64_t w = L.word[j] ? keys_hi[c] : keys[c];
+      const int bits = L.bits[j];
+      const uint64_t f = (w >> L.shift[j]) & (bits >= 64 ? ~0ull : ((1ull << bits) - 1));
+      out[c * L.k + j] = int64_t(f) - 1 + L.cmin[j];
     }
   }
 }
@@ -248,19 +253,18 @@ int tj_grid_export(tj_ctx* ctx, uint32_t* point_order, int64_t* cell_start, int6
       TJ_CUDA(cudaMemcpy(runs, ctx->runs.ptr, sizeof(uint2) * g.n_runs, cudaMemcpyDeviceToHost));
     if (cell_coords) {
       DevBuf tmp;
-      tmp.ensure(sizeof(int64_t) * g.n_cells * g.k + 128 * 2, s);
-      int* dshift = reinterpret_cast<int*>(tmp.as<char>() + sizeof(int64_t) * g.n_cells * g.k);
-      long long* dcmin = reinterpret_cast<long long*>(dshift + 16);
-      int hshift[TJ_MAX_K_IDX];
-      long long hcmin[TJ_MAX_K_IDX];
+      tmp.ensure(sizeof(int64_t) * g.n_cells * g.k, s);
+      KeyLayout L{};
+      L.k = g.k;
       for (int j = 0; j < g.k; ++j) {
-        hshift[j] = g.shift[j];
-        hcmin[j] = g.cmin[j];
+        L.shift[j] = g.shift[j];
+        L.bits[j] = g.bits[j];
+        L.word[j] = g.word[j];
+        L.cmin[j] = g.cmin[j];
       }
-      TJ_CUDA(cudaMemcpyAsync(dshift, hshift, sizeof(int) * g.k, cudaMemcpyHostToDevice, s));
-      TJ_CUDA(cudaMemcpyAsync(dcmin, hcmin, sizeof(long long) * g.k, cudaMemcpyHostToDevice, s));
-      decode_keys_kernel<<<256, 256, 0, s>>>(ctx->cell_key.as<uint64_t>(), g.n_cells, g.k, dshift,
-                                             dcmin, tmp.as<int64_t>());
+      decode_keys_kernel<<<256, 256, 0, s>>>(ctx->cell_key.as<uint64_t>(),
+                                             g.wide ? ctx->cell_key_hi.as<uint64_t>() : nullptr,
+                                             g.n_cells, L, tmp.as<int64_t>());
       TJ_CHECK_LAUNCH();
       TJ_CUDA(cudaMemcpyAsync(cell_coords, tmp.ptr, sizeof(int64_t) * g.n_cells * g.k,
                               cudaMemcpyDeviceToHost, s));

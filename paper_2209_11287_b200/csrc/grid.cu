@@ -26,6 +26,7 @@ namespace tj {
 struct KeyParams {
   int k;
   int shift[TJ_MAX_K_IDX];
+  int word[TJ_MAX_K_IDX];
   long long cmin[TJ_MAX_K_IDX];
 };
 
@@ -134,6 +135,36 @@ __global__ void cell_key_kernel(const double* __restrict__ x, int64_t n, int ld,
   }
 }
 
+// Two-word cell keys (> 63 bits): dims with word 1 in `hi`, the rest in `lo`;
+// row i of x, or row perm[i] when perm is given (the keys in sorted order).
+__global__ void cell_key2_kernel(const double* __restrict__ x, int64_t n, int ld, double eps,
+                                 KeyParams kp, const uint32_t* __restrict__ perm,
+                                 uint64_t* __restrict__ lo, uint64_t* __restrict__ hi) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = perm ? int64_t(perm[i]) : i;
+    uint64_t kl = 0, kh = 0;
+#pragma unroll
+    for (int j = 0; j < TJ_MAX_K_IDX; ++j) {
+      if (j < kp.k) {
+        const long long c = cell_coord(x[row * ld + j], eps);
+        const uint64_t f = uint64_t(c - kp.cmin[j] + 1) << kp.shift[j];
+        if (kp.word[j]) kh |= f;
+        else kl |= f;
+      }
+    }
+    lo[i] = kl;
+    hi[i] = kh;
+  }
+}
+
+__global__ void gather_u64_kernel(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx,
+                                  int64_t n, uint64_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
 // Cell-ordered zero-padded coordinates, chunk norms in the reference order
 // ((((0+x0^2)+x1^2)+x2^2)+x3^2 per chunk, kernels.py:126-130) and full norms.
 // One chunk (d <= 4): the chunk norm is the norm, CN is not written (only the
@@ -145,8 +176,9 @@ __global__ void permute_kernel(const double* __restrict__ x, int64_t n, int ld, 
                                unsigned long long* max_norm_bits) {
   const int nchunks = d_pad / 4;
   unsigned long long local_max = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n;
-       p += int64_t(gridDim.x) * blockDim.x) {
+       p += stride) {
     const int64_t id = perm[p];
     const double* src = x + id * ld;
     double* dst = P + p * d_pad;
@@ -219,6 +251,53 @@ struct CellTableOut {
   }
 };
 
+struct HeadFlag2 {
+  const uint64_t* lo;
+  const uint64_t* hi;
+  __device__ int64_t operator()(int64_t i) const {
+    return i == 0 || lo[i] != lo[i - 1] || hi[i] != hi[i - 1];
+  }
+};
+struct CellTableOut2 {
+  const uint64_t* lo;
+  const uint64_t* hi;
+  uint64_t* cell_key;
+  uint64_t* cell_key_hi;
+  int64_t* cell_start;
+  __device__ void operator()(int64_t i, int64_t excl) const {
+    if (i == 0 || lo[i] != lo[i - 1] || hi[i] != hi[i - 1]) {
+      cell_key[excl] = lo[i];
+      cell_key_hi[excl] = hi[i];
+      cell_start[excl] = i;
+    }
+  }
+};
+
+// (hi, lo) lexicographic bounds over the two-word cell keys.
+__device__ __forceinline__ bool key2_less(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+__device__ __forceinline__ int64_t lower_bound_key2(const uint64_t* kh, const uint64_t* kl,
+                                                    int64_t n, uint64_t vh, uint64_t vl) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key2_less(kh[mid], kl[mid], vh, vl)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t upper_bound_key2(const uint64_t* kh, const uint64_t* kl,
+                                                    int64_t n, uint64_t vh, uint64_t vl) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (!key2_less(vh, vl, kh[mid], kl[mid])) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
   int64_t lo = 0, hi = n;
   while (lo < hi) {
@@ -247,6 +326,9 @@ struct RowParams {
   const int* dense;
   long long dstride[TJ_MAX_K_IDX];
   unsigned long long fmask[TJ_MAX_K_IDX];
+  // two-word keys: high words of the cell keys (null: one word), word of each dim
+  const uint64_t* key_hi;
+  int word[TJ_MAX_K_IDX];
 };
 
 __device__ __forceinline__ long long dense_index(const RowParams& rp, uint64_t key) {
@@ -256,7 +338,8 @@ __device__ __forceinline__ long long dense_index(const RowParams& rp, uint64_t k
 }
 
 // Position range [b, e) of neighbour row r of the cell with key `key`.
-__device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key, int r,
+__device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key, uint64_t key_hi,
+                                              int r,
                                               const uint64_t* cell_key, const int64_t* cell_start,
                                               int64_t n_cells, int64_t& b, int64_t& e) {
   if (rp.dense) {
@@ -278,14 +361,23 @@ __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key,
     }
     return;
   }
-  long long delta = 0;
+  long long delta = 0, delta_hi = 0;
   int rr = r;
   for (int j = rp.k - 2; j >= 0; --j) {  // dim k-2 is the fastest-varying digit
     const int o = rr % 3 - 1;
     rr /= 3;
-    delta += (long long)o << rp.shift[j];
+    if (rp.word[j]) delta_hi += (long long)o << rp.shift[j];
+    else delta += (long long)o << rp.shift[j];
   }
-  const uint64_t last = 1ull << rp.shift[rp.k - 1];
+  const uint64_t last = 1ull << rp.shift[rp.k - 1];  // dim k-1 is always in the low word
+  if (rp.key_hi) {  // fields never carry into each other (coordinates are offset by 1)
+    const uint64_t kh = key_hi + uint64_t(delta_hi);
+    const int64_t a = lower_bound_key2(rp.key_hi, cell_key, n_cells, kh, key + uint64_t(delta) - last);
+    const int64_t z = upper_bound_key2(rp.key_hi, cell_key, n_cells, kh, key + uint64_t(delta) + last);
+    b = cell_start[a];
+    e = cell_start[z];
+    return;
+  }
   const uint64_t lo_key = key + uint64_t(delta) - last;
   const uint64_t hi_key = key + uint64_t(delta) + last;
   const int64_t a = lower_bound_u64(cell_key, n_cells, lo_key);
@@ -367,7 +459,8 @@ __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cel
     int64_t runs = 0, cands = 0;
     for (int r = lane_id(); r < rp.n_rows; r += 32) {
       int64_t b, e;
-      neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
+      neighbour_row(rp, key, rp.key_hi ? rp.key_hi[c] : 0ull, r, cell_key, cell_start, n_cells, b,
+                    e);
       if (e > b) {
         runs += 1;
         cands += e - b;
@@ -426,7 +519,9 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
     for (int r0 = 0; r0 < rp.n_rows; r0 += 32) {
       const int r = r0 + lane_id();
       int64_t b = 0, e = 0;
-      if (r < rp.n_rows) neighbour_row(rp, key, r, cell_key, cell_start, n_cells, b, e);
+      if (r < rp.n_rows)
+        neighbour_row(rp, key, rp.key_hi ? rp.key_hi[c] : 0ull, r, cell_key, cell_start, n_cells,
+                      b, e);
       const unsigned m = __ballot_sync(0xffffffffu, e > b);
       const int64_t len = e - b;
       const int64_t inc = warp_inclusive_scan(len);
@@ -527,14 +622,29 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
     total_bits += b;
     g.cmin[j] = hmm[2 * j];
   }
-  if (total_bits > 63)
-    fail(TJ_EINVAL, "cell key over k_idx=" + std::to_string(k) + " indexed dimensions needs " +
-                        std::to_string(total_bits) +
-                        " bits (> 63); use a smaller k_idx or a larger epsilon");
-  int sh = 0;
-  for (int j = k - 1; j >= 0; --j) {
-    g.shift[j] = sh;
-    sh += bits[j];
+  g.wide = total_bits > 63;
+  for (int j = 0; j < k; ++j) g.bits[j] = bits[j];
+  {
+    // dim 0 most significant; one word when the key fits in 63 bits, else the
+    // last dims fill the low word and the rest go to the high word
+    int sh = 0, j = k - 1;
+    for (; j >= 0 && (!g.wide || sh + bits[j] <= 63); --j) {
+      g.shift[j] = sh;
+      g.word[j] = 0;
+      sh += bits[j];
+    }
+    g.lo_bits = sh;
+    sh = 0;
+    for (; j >= 0; --j) {
+      if (sh + bits[j] > 63)
+        fail(TJ_EINVAL, "cell key over k_idx=" + std::to_string(k) + " indexed dimensions needs " +
+                            std::to_string(total_bits) +
+                            " bits (> 126); use a smaller k_idx or a larger epsilon");
+      g.shift[j] = sh;
+      g.word[j] = 1;
+      sh += bits[j];
+    }
+    g.hi_bits = sh;
   }
   g.key_bits = total_bits;
 
@@ -547,6 +657,7 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   kp.k = k;
   for (int j = 0; j < k; ++j) {
     kp.shift[j] = g.shift[j];
+    kp.word[j] = g.word[j];
     kp.cmin[j] = g.cmin[j];
   }
   const int64_t hist_elems = radix_sort_scratch_elems(n);
@@ -554,7 +665,33 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   ScanScratch sc = scan_scratch(ctx, std::max<int64_t>(hist_elems, n), s);
   ctx->cell_key.ensure(sizeof(uint64_t) * (n + 1), s);
   ctx->cell_start.ensure(sizeof(int64_t) * (n + 1), s);
-  if (total_bits <= 32) {
+  if (g.wide) {
+    // lo word first, then the hi word (stable), as two LSD sorts; the sorted
+    // keys are recomputed from the coordinates in the final order
+    uint64_t* k0 = ctx->keys.as<uint64_t>();
+    uint64_t* k1 = ctx->keys_alt.as<uint64_t>();
+    ctx->keys_hi.ensure(sizeof(uint64_t) * n, s);
+    ctx->cell_key_hi.ensure(sizeof(uint64_t) * (n + 1), s);
+    uint64_t* kh = ctx->keys_hi.as<uint64_t>();
+    cell_key2_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, nullptr, k0, kh);
+    TJ_CHECK_LAUNCH();
+    const int w1 = radix_sort_pairs(k0, ctx->perm.as<uint32_t>(), k1, ctx->vals_alt.as<uint32_t>(),
+                                    n, g.lo_bits, true, ctx->sort_hist.as<int64_t>(), sc, s);
+    uint32_t* pa = w1 ? ctx->vals_alt.as<uint32_t>() : ctx->perm.as<uint32_t>();
+    uint32_t* pb = w1 ? ctx->perm.as<uint32_t>() : ctx->vals_alt.as<uint32_t>();
+    gather_u64_kernel<<<grid_for(n, 256), 256, 0, s>>>(kh, pa, n, k0);
+    TJ_CHECK_LAUNCH();
+    const int w2 = radix_sort_pairs(k0, pa, k1, pb, n, g.hi_bits, false,
+                                    ctx->sort_hist.as<int64_t>(), sc, s);
+    if ((w2 ? pb : pa) != ctx->perm.as<uint32_t>()) std::swap(ctx->perm, ctx->vals_alt);
+    cell_key2_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, ctx->perm.as<uint32_t>(),
+                                                       k0, kh);
+    TJ_CHECK_LAUNCH();
+    scan_exclusive(HeadFlag2{k0, kh},
+                   CellTableOut2{k0, kh, ctx->cell_key.as<uint64_t>(),
+                                 ctx->cell_key_hi.as<uint64_t>(), ctx->cell_start.as<int64_t>()},
+                   n, sc, s);
+  } else if (total_bits <= 32) {
     uint32_t* k0 = ctx->keys.as<uint32_t>();
     uint32_t* k1 = ctx->keys_alt.as<uint32_t>();
     cell_key_kernel<uint32_t><<<grid_for(n, 256), 256, 0, s>>>(x, n, ld, eps, kp, k0);
@@ -616,7 +753,11 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
   rp.k = k;
   rp.n_rows = 1;
   for (int j = 0; j < k - 1; ++j) rp.n_rows *= 3;
-  for (int j = 0; j < k; ++j) rp.shift[j] = g.shift[j];
+  for (int j = 0; j < k; ++j) {
+    rp.shift[j] = g.shift[j];
+    rp.word[j] = g.word[j];
+  }
+  rp.key_hi = g.wide ? ctx->cell_key_hi.as<uint64_t>() : nullptr;
   const int64_t nc = g.n_cells;
   // dense box lookup when the guarded box is small (<= max(8 * cells, 4M) entries)
   {
@@ -624,13 +765,13 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
     bool small = true;
     for (int j = k - 1; j >= 0; --j) {
       rp.dstride[j] = box;
-      const int fbits = (j == 0 ? g.key_bits : g.shift[j - 1]) - g.shift[j];
+      const int fbits = g.bits[j];
       rp.fmask[j] = fbits >= 64 ? ~0ull : (1ull << fbits) - 1;
       const long long span = (long long)(hmm[2 * j + 1] - hmm[2 * j]) + 3;  // fields 0..range+2
       if (box > (1ll << 40) / span) small = false;
       else box *= span;
     }
-    if (small && box <= std::max<long long>(8 * nc, 1ll << 22)) {
+    if (!g.wide && small && box <= std::max<long long>(8 * nc, 1ll << 22)) {
       ctx->dense.ensure(sizeof(int) * box, s);
       TJ_CUDA(cudaMemsetAsync(ctx->dense.ptr, 0xff, sizeof(int) * box, s));
       rp.dense = ctx->dense.as<int>();

@@ -107,7 +107,12 @@ struct GridState {
   int d = 0, d_pad = 0, k = 0, nchunks = 0;
   double eps = 0, eps_sq = 0;
   int key_bits = 0;
-  int shift[TJ_MAX_K_IDX] = {};
+  // cell keys wider than 63 bits: two words, dims [0, split) in the high word
+  bool wide = false;
+  int lo_bits = 0, hi_bits = 0;
+  int bits[TJ_MAX_K_IDX] = {};
+  int word[TJ_MAX_K_IDX] = {};     // 0: low word, 1: high word
+  int shift[TJ_MAX_K_IDX] = {};    // inside the dim's word
   int64_t cmin[TJ_MAX_K_IDX] = {};
   int64_t n_cells = 0, n_runs = 0, candidates = 0, tiles = 0, max_cell = 0;
   double max_norm = 0;
@@ -121,7 +126,7 @@ struct tj_ctx {
   cudaStream_t last_stream = nullptr;
   tj::GridState g;
   // grid buffers
-  tj::DevBuf P, NRM, CN, perm, keys, cell_key, cell_start, cell_runs, runs, run_off, cell_cand,
+  tj::DevBuf P, NRM, CN, perm, keys, keys_hi, cell_key, cell_key_hi, cell_start, cell_runs, runs, run_off, cell_cand,
       cell_cost, dense, SFX;
   // scratch
   tj::DevBuf keys_alt, vals_alt, sort_hist, scan_partial, scan_total, minmax, tmp64, items;

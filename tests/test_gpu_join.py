@@ -288,6 +288,34 @@ def test_grid_candidates_match_oracle():
             assert got == expect
 
 
+def _wide_key_dataset():
+    """6-D points whose cell key needs > 63 bits (a far cluster stretches
+    every indexed dim to ~14 bits): the device grid packs two words."""
+    rng = np.random.default_rng(11)
+    x = rng.random((4000, 6)) * 0.6
+    x[:7] += 1e3
+    x[7:11] -= 1e3
+    return Dataset(x)
+
+
+def test_wide_cell_keys_grid_matches_oracle():
+    ds, eps = _wide_key_dataset(), 0.12
+    idx = tgrid.build_index(ds, eps, 6)
+    order, cstart, ccoord, cand = oracle.grid(ds, eps, 6)
+    assert np.array_equal(idx.point_order, order.astype(np.int64))
+    assert [tuple(c) for c in ccoord.tolist()] == idx.ordered_cells
+    assert np.array_equal(idx.cell_cands, cand)
+
+
+@pytest.mark.parametrize("kernel", ALL_KERNELS)
+def test_wide_cell_keys_join(kernel):
+    ds, eps = _wide_key_dataset(), 0.12
+    r = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, k_idx=6))
+    assert_oracle_equal(r, ds, eps, k_idx=6)
+    s = self_join(ds, JoinConfig(epsilon=eps, kernel=kernel, k_idx=5))  # 75 bits over 5 dims
+    assert_oracle_equal(s, ds, eps, k_idx=5)
+
+
 # -------------------------------------------------------------- edge cases
 
 

@@ -14,5 +14,10 @@ python tools/launch_summary.py "$out/launches_c5.csv" > "$out/launches_c5_summar
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file "$out/launches_c2.csv" python tools/index_probe.py c2 2 > "$out/ncu_c2.log" 2>&1
 python tools/launch_summary.py "$out/launches_c2.csv" > "$out/launches_c2_summary.txt" 2>&1
+for c in c3 expo3d2m; do
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file "$out/launches_$c.csv" python tools/index_probe.py $c 2 > "$out/ncu_$c.log" 2>&1
+  python tools/launch_summary.py "$out/launches_$c.csv" > "$out/launches_${c}_summary.txt" 2>&1
+done
 timeout 600 python bench.py --skip-cpu > "$out/bench.json" 2> "$out/bench.err"; echo "bench rc=$?" >> "$out/status.txt"
 cat "$out/status.txt" "$out/index.txt"; head -12 "$out/launches_c5_summary.txt"; head -12 "$out/launches_c2_summary.txt"
