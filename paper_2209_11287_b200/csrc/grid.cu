@@ -321,9 +321,10 @@ struct RowParams {
   int k;
   int n_rows;                     // 3^(k-1)
   long long shift[TJ_MAX_K_IDX];  // as 64-bit for the offset arithmetic
-  // Dense cell lookup (when the guarded coordinate box is small): cell index per
-  // mixed-radix box index, -1 when empty.  Null: binary search on cell_key.
-  const int* dense;
+  // Dense cell lookup (when the guarded coordinate box is small): the position
+  // range {start, end} of the cell at each mixed-radix box index, {~0, ~0} when
+  // empty (one dependent load to a row's range).  Null: binary search on cell_key.
+  const uint2* dense;
   long long dstride[TJ_MAX_K_IDX];
   unsigned long long fmask[TJ_MAX_K_IDX];
   // two-word keys: high words of the cell keys (null: one word), word of each dim
@@ -335,6 +336,19 @@ __device__ __forceinline__ long long dense_index(const RowParams& rp, uint64_t k
   long long idx = 0;
   for (int j = 0; j < rp.k; ++j) idx += (long long)((key >> rp.shift[j]) & rp.fmask[j]) * rp.dstride[j];
   return idx;
+}
+
+// Position range of the three box entries of a row (left to right along the last dim).
+__device__ __forceinline__ void dense_range(uint2 c0, uint2 c1, uint2 c2, int64_t& b, int64_t& e) {
+  constexpr uint32_t kEmpty = 0xffffffffu;
+  const uint32_t first = c0.x != kEmpty ? c0.x : (c1.x != kEmpty ? c1.x : c2.x);
+  const uint32_t last = c2.x != kEmpty ? c2.y : (c1.x != kEmpty ? c1.y : c0.y);
+  if (first == kEmpty) {
+    b = e = 0;
+  } else {
+    b = first;
+    e = last;
+  }
 }
 
 // Position range [b, e) of neighbour row r of the cell with key `key`.
@@ -350,15 +364,8 @@ __device__ __forceinline__ void neighbour_row(const RowParams& rp, uint64_t key,
       idx += (long long)(rr % 3 - 1) * rp.dstride[j];
       rr /= 3;
     }
-    const int c0 = rp.dense[idx - 1], c1 = rp.dense[idx], c2 = rp.dense[idx + 1];
-    const int first = c0 >= 0 ? c0 : (c1 >= 0 ? c1 : c2);
-    const int last = c2 >= 0 ? c2 : (c1 >= 0 ? c1 : c0);
-    if (first < 0) {
-      b = e = 0;
-    } else {
-      b = cell_start[first];
-      e = cell_start[last + 1];
-    }
+    const uint2 c0 = rp.dense[idx - 1], c1 = rp.dense[idx], c2 = rp.dense[idx + 1];
+    dense_range(c0, c1, c2, b, e);
     return;
   }
   long long delta = 0, delta_hi = 0;
@@ -399,26 +406,76 @@ __device__ __forceinline__ void dense_rows(const RowParams& rp, const uint64_t (
     delta += (long long)(rr % 3 - 1) * rp.dstride[j];
     rr /= 3;
   }
-  int cc[U][3];
+  uint2 cc[U][3];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const long long idx = dense_index(rp, key[u]) + delta;
 #pragma unroll
     for (int t = 0; t < 3; ++t) cc[u][t] = __ldg(rp.dense + idx - 1 + t);
   }
-  int64_t sb[U], se[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int first = cc[u][0] >= 0 ? cc[u][0] : (cc[u][1] >= 0 ? cc[u][1] : cc[u][2]);
-    const int last = cc[u][2] >= 0 ? cc[u][2] : (cc[u][1] >= 0 ? cc[u][1] : cc[u][0]);
-    sb[u] = first >= 0 ? __ldg(cell_start + first) : 0;
-    se[u] = first >= 0 ? __ldg(cell_start + last + 1) : 0;
+  for (int u = 0; u < U; ++u) dense_range(cc[u][0], cc[u][1], cc[u][2], b[u], e[u]);
+}
+
+// Galloping searches: the same neighbour row of consecutive cells (ascending
+// keys) has non-decreasing bounds, so a warp that walks a contiguous range of
+// cells starts every search at the row's previous answer (a few probes instead
+// of a full binary search).
+// first i >= from with a[i] >= v; a[from - 1] < v
+__device__ __forceinline__ int64_t gallop_lb(const uint64_t* __restrict__ a, int64_t n, uint64_t v,
+                                             int64_t from) {
+  if (from >= n || a[from] >= v) return from;
+  int64_t lo = from, hi = from + 1, step = 1;  // a[lo] < v
+  while (hi < n && a[hi] < v) {
+    lo = hi;
+    step <<= 1;
+    hi = from + step;
   }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    b[u] = sb[u];
-    e[u] = se[u];
+  if (hi > n) hi = n;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid;
+    else hi = mid;
   }
+  return hi;
+}
+// first i >= from with a[i] > v; a[from - 1] <= v
+__device__ __forceinline__ int64_t gallop_ub(const uint64_t* __restrict__ a, int64_t n, uint64_t v,
+                                             int64_t from) {
+  if (from >= n || a[from] > v) return from;
+  int64_t lo = from, hi = from + 1, step = 1;  // a[lo] <= v
+  while (hi < n && a[hi] <= v) {
+    lo = hi;
+    step <<= 1;
+    hi = from + step;
+  }
+  if (hi > n) hi = n;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid;
+    else hi = mid;
+  }
+  return hi;
+}
+
+// Key range [lo, hi] of neighbour row r (one-word keys).
+__device__ __forceinline__ void row_key_range(const RowParams& rp, uint64_t key, int r,
+                                              uint64_t& lo, uint64_t& hi) {
+  long long delta = 0;
+  int rr = r;
+  for (int j = rp.k - 2; j >= 0; --j) {
+    delta += (long long)(rr % 3 - 1) << rp.shift[j];
+    rr /= 3;
+  }
+  const uint64_t last = 1ull << rp.shift[rp.k - 1];
+  lo = key + uint64_t(delta) - last;
+  hi = key + uint64_t(delta) + last;
+}
+
+constexpr int kGallopSlots = 8;  // rows per lane: k_idx <= 6 (243 rows)
+
+__device__ __forceinline__ bool use_gallop(const RowParams& rp) {
+  return !rp.dense && !rp.key_hi && rp.n_rows <= 32 * kGallopSlots;
 }
 
 constexpr int kCandU = 4;  // cells per warp iteration (dense lookup)
@@ -450,6 +507,41 @@ __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cel
           run_count[c0 + u] = runs;
           cand_count[c0 + u] = cands;
         }
+      }
+    }
+    return;
+  }
+  if (use_gallop(rp)) {  // contiguous cells per warp, galloping row searches
+    const int64_t per = (n_cells + warps - 1) / warps;
+    const int64_t cb = w0 * per, ce = min(n_cells, cb + per);
+    int64_t pa[kGallopSlots], pz[kGallopSlots];
+#pragma unroll
+    for (int i = 0; i < kGallopSlots; ++i) pa[i] = pz[i] = 0;
+    for (int64_t c = cb; c < ce; ++c) {
+      const uint64_t key = cell_key[c];
+      int64_t runs = 0, cands = 0;
+#pragma unroll
+      for (int i = 0; i < kGallopSlots; ++i) {
+        const int r = int(lane_id()) + 32 * i;
+        if (r < rp.n_rows) {
+          uint64_t lo, hi;
+          row_key_range(rp, key, r, lo, hi);
+          const int64_t a = gallop_lb(cell_key, n_cells, lo, pa[i]);
+          const int64_t z = gallop_ub(cell_key, n_cells, hi, max(pz[i], a));
+          pa[i] = a;
+          pz[i] = z;
+          const int64_t b = cell_start[a], e = cell_start[z];
+          if (e > b) {
+            runs += 1;
+            cands += e - b;
+          }
+        }
+      }
+      runs = warp_sum(runs);
+      cands = warp_sum(cands);
+      if (lane_id() == 0) {
+        run_count[c] = runs;
+        cand_count[c] = cands;
       }
     }
     return;
@@ -512,6 +604,44 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
     }
     return;
   }
+  if (use_gallop(rp)) {
+    const int64_t per = (n_cells + warps - 1) / warps;
+    const int64_t cb = w0 * per, ce = min(n_cells, cb + per);
+    int64_t pa[kGallopSlots], pz[kGallopSlots];
+#pragma unroll
+    for (int i = 0; i < kGallopSlots; ++i) pa[i] = pz[i] = 0;
+    for (int64_t c = cb; c < ce; ++c) {
+      const uint64_t key = cell_key[c];
+      int64_t out = cell_runs[c];
+      int64_t off = 0;
+#pragma unroll
+      for (int i = 0; i < kGallopSlots; ++i) {
+        if (32 * i >= rp.n_rows) break;
+        const int r = int(lane_id()) + 32 * i;
+        int64_t b = 0, e = 0;
+        if (r < rp.n_rows) {
+          uint64_t lo, hi;
+          row_key_range(rp, key, r, lo, hi);
+          const int64_t a = gallop_lb(cell_key, n_cells, lo, pa[i]);
+          const int64_t z = gallop_ub(cell_key, n_cells, hi, max(pz[i], a));
+          pa[i] = a;
+          pz[i] = z;
+          b = cell_start[a];
+          e = cell_start[z];
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, e > b);
+        const int64_t len = e - b;
+        const int64_t inc = warp_inclusive_scan(len);
+        if (e > b) {
+          runs[out + __popc(m & lt)] = make_uint2(uint32_t(b), uint32_t(e));
+          run_off[out + __popc(m & lt)] = uint32_t(off + inc - len);
+        }
+        out += __popc(m);
+        off += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    return;
+  }
   for (int64_t c = w0; c < n_cells; c += warps) {
     const uint64_t key = cell_key[c];
     int64_t out = cell_runs[c];
@@ -536,10 +666,11 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
 }
 
 __global__ void dense_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell_key,
-                                  int64_t n_cells, int* __restrict__ dense) {
+                                  const int64_t* __restrict__ cell_start, int64_t n_cells,
+                                  uint2* __restrict__ dense) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
        c += int64_t(gridDim.x) * blockDim.x)
-    dense[dense_index(rp, cell_key[c])] = int(c);
+    dense[dense_index(rp, cell_key[c])] = make_uint2(uint32_t(cell_start[c]), uint32_t(cell_start[c + 1]));
 }
 
 // cost = |cell|*|cand|, tiles = ceil(|cell|/8)*ceil(|cand|/8) (join.py:170-173, 257-261).
@@ -772,11 +903,12 @@ void build_grid(tj_ctx* ctx, const double* x, int64_t n, int d, int64_t ld64, in
       else box *= span;
     }
     if (!g.wide && small && box <= std::max<long long>(8 * nc, 1ll << 22)) {
-      ctx->dense.ensure(sizeof(int) * box, s);
-      TJ_CUDA(cudaMemsetAsync(ctx->dense.ptr, 0xff, sizeof(int) * box, s));
-      rp.dense = ctx->dense.as<int>();
-      dense_fill_kernel<<<grid_for(nc, 256), 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(), nc,
-                                                          ctx->dense.as<int>());
+      ctx->dense.ensure(sizeof(uint2) * box, s);
+      TJ_CUDA(cudaMemsetAsync(ctx->dense.ptr, 0xff, sizeof(uint2) * box, s));
+      rp.dense = ctx->dense.as<uint2>();
+      dense_fill_kernel<<<grid_for(nc, 256), 256, 0, s>>>(rp, ctx->cell_key.as<uint64_t>(),
+                                                          ctx->cell_start.as<int64_t>(), nc,
+                                                          ctx->dense.as<uint2>());
       TJ_CHECK_LAUNCH();
     } else {
       rp.dense = nullptr;
