@@ -12,7 +12,7 @@
 //    scan in position order places the rows), then sort_rows_kernel reads 32
 //    consecutive staging rows (coalesced), sorts one row per lane and writes
 //    each row to its final place.
-//  Rows longer than 96 ids are sorted in place by a warp (<= 256), one CTA
+//  Rows longer than 88 ids are sorted in place by a warp (<= 256), one CTA
 //  (shared-memory bitonic, <= 8192) or, beyond that, by a composite-key radix
 //  sort.
 #include "internal.cuh"
@@ -111,7 +111,7 @@ constexpr int kBlockSortMax = 8192;
 // data-dependent min/max pairs (N = 64: 543 comparators, ~34 warp
 // instructions per row when the warp is full) -- versus ~300 for a warp-wide
 // bitonic sort of the same row.
-constexpr int kPoolSlots = 96;
+constexpr int kPoolSlots = 88;
 constexpr int kPoolLd = 33;
 
 // Comparator list of Batcher's odd-even merge sort for N keys (the network of
@@ -183,7 +183,7 @@ __device__ __noinline__ void pool_sort(uint32_t* pool, int len) {
   // the straight-line code stays resident in the instruction cache
   if (mx <= 32) pool_sort_n<32>(pool, len);
   else if (mx <= 64) pool_sort_n<64>(pool, len);
-  else pool_sort_n<96>(pool, len);
+  else pool_sort_n<88>(pool, len);
 }
 
 // Rows with more than kPoolSlots ids are written straight to their place and
@@ -498,7 +498,7 @@ __device__ __forceinline__ uint32_t run_position(const uint2* __restrict__ runs,
 // kEmitCells cells), positions to original ids with 16 gathers in flight; the
 // warp sorts the 32 rows in registers (odd-even merge network per lane) and
 // writes them to their places.  Longer rows are listed for long_rows_kernel.
-constexpr int kEmitWarps = 4;
+constexpr int kEmitWarps = 2;
 constexpr int kEmitCells = 8;   // cells of one window whose run tables are staged
 constexpr int kRunTab = 32;     // >= 27 runs (k <= 4) + the list-length sentinel
 constexpr int kBlkTab = 256;    // block -> run hints per staged cell (2048 candidates)
@@ -1115,7 +1115,7 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
   ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
   uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
   if (le > lb) {
-    auto kern = emit_rows_kernel<4, true>;
+    auto kern = emit_rows_kernel<7, true>;
     const size_t smem = sizeof(EmitSmem) * kEmitWarps;
     TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
@@ -1175,7 +1175,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     {
       // 4 CTAs/SM (<= 128 registers): measured on par with the unbounded build
       // (158 registers, 3 CTAs) and well ahead of 5 CTAs (spills)
-      auto kern = emit_rows_kernel<4, false>;
+      auto kern = emit_rows_kernel<7, false>;
       const size_t smem = sizeof(EmitSmem) * kEmitWarps;
       TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
