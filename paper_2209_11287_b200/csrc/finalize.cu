@@ -499,7 +499,7 @@ __device__ __forceinline__ uint32_t run_position(const uint2* __restrict__ runs,
 // warp sorts the 32 rows in registers (odd-even merge network per lane) and
 // writes them to their places.  Longer rows are listed for long_rows_kernel.
 constexpr int kEmitWarps = 2;
-constexpr int kEmitCells = 8;   // cells of one window whose run tables are staged
+constexpr int kEmitCells = 4;   // cells of one window whose run tables are staged
 constexpr int kRunTab = 32;     // >= 27 runs (k <= 4) + the list-length sentinel
 constexpr int kBlkTab = 256;    // block -> run hints per staged cell (2048 candidates)
 
@@ -1115,7 +1115,7 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
   ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
   uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
   if (le > lb) {
-    auto kern = emit_rows_kernel<7, true>;
+    auto kern = emit_rows_kernel<8, true>;
     const size_t smem = sizeof(EmitSmem) * kEmitWarps;
     TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
@@ -1175,7 +1175,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     {
       // 4 CTAs/SM (<= 128 registers): measured on par with the unbounded build
       // (158 registers, 3 CTAs) and well ahead of 5 CTAs (spills)
-      auto kern = emit_rows_kernel<7, false>;
+      auto kern = emit_rows_kernel<8, false>;
       const size_t smem = sizeof(EmitSmem) * kEmitWarps;
       TJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
