@@ -634,11 +634,29 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
           while (ro[r + 1] <= t) ++r;
           col[i * kPoolLd] = rp[r] + (t - ro[r]);
         }
-      } else {  // many tiny cells in the window, or a very long list: global search
+      } else {
+        // many cells in the window (small cells, or a position list), or a very
+        // long list: walk the cell's run table in global memory from the previous
+        // hit's run (offsets come out nearly ascending: a step or two per hit)
         const int64_t rb = cell_runs[c];
         const int nr = int(cell_runs[c + 1] - rb);
-        for (int i = 0; i < nf; ++i)
-          col[i * kPoolLd] = run_position(runs, run_off, rb, nr, col[i * kPoolLd]);
+        const uint32_t* ro = run_off + rb;
+        int r = 0;
+        uint32_t r_lo = __ldg(ro), r_hi = nr > 1 ? __ldg(ro + 1) : 0xffffffffu;
+        for (int i = 0; i < nf; ++i) {
+          const uint32_t t = col[i * kPoolLd];
+          while (t >= r_hi) {
+            ++r;
+            r_lo = r_hi;
+            r_hi = r + 1 < nr ? __ldg(ro + r + 1) : 0xffffffffu;
+          }
+          while (t < r_lo) {
+            --r;
+            r_hi = r_lo;
+            r_lo = __ldg(ro + r);
+          }
+          col[i * kPoolLd] = runs[rb + r].x + (t - r_lo);
+        }
       }
       // 3. symmetric join: positions of the pairs with earlier neighbour cells,
       //    from their masks
