@@ -205,6 +205,7 @@ __global__ void route_tile_count_kernel(const unsigned long long* __restrict__ d
   }
 }
 
+template <bool VEC>
 __global__ void route_tile_write_kernel(const unsigned long long* __restrict__ dest, int64_t n,
                                         int G, int64_t n_tiles, const int64_t* __restrict__ tile_off,
                                         const double* __restrict__ x, int64_t ld, int d,
@@ -230,7 +231,12 @@ __global__ void route_tile_write_kernel(const unsigned long long* __restrict__ d
           const int64_t o = at + __popc(bal & lt);
           const double* src = x + i * ld;
           double* dst = out + o * ld_out;
-          for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
+          if (VEC) {  // rows of d == ld == ld_out doubles, 16-byte aligned
+            for (int j = 0; j < ld_out; j += 2)
+              *reinterpret_cast<double2*>(dst + j) = __ldg(reinterpret_cast<const double2*>(src + j));
+          } else {
+            for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
+          }
           gid[o] = uint32_t(gid_base + i);
         }
         at += __popc(bal);
@@ -416,8 +422,11 @@ void shard_route(tj_ctx* ctx, const double* x, int64_t n, int64_t ld, int d, int
   TJ_CHECK_LAUNCH();
   ScanScratch sc = scan_scratch(ctx, G * n_tiles, s);
   scan_exclusive(LoadAt<int64_t>{tiles}, StoreAt<int64_t>{tiles}, G * n_tiles, sc, s);
-  route_tile_write_kernel<<<warp_grid, 256, 0, s>>>(dest, n, G, n_tiles, tiles, x, ld, d, out, ld_out,
-                                                    gid, gid_base);
+  // unpadded even-width rows copy as double2
+  const bool vec = ld == ld_out && ld % 2 == 0 && d == ld &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  auto write = vec ? route_tile_write_kernel<true> : route_tile_write_kernel<false>;
+  write<<<warp_grid, 256, 0, s>>>(dest, n, G, n_tiles, tiles, x, ld, d, out, ld_out, gid, gid_base);
   TJ_CHECK_LAUNCH();
 }
 

@@ -18,6 +18,8 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#include <cstdlib>
+
 namespace tj {
 
 constexpr int kSortThreads = 256;
@@ -26,6 +28,7 @@ constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 keys
 constexpr int kSortWarps = kSortThreads / kWarp;
 constexpr int kSortWarpKeys = kSortRounds * kWarp;     // 512 consecutive keys per warp
 constexpr int kMaxDigitBits = 11;
+constexpr int kDefaultDigitBits = 10;
 
 template <class K>
 __device__ __forceinline__ unsigned digit_of(K key, int shift, unsigned mask) {
@@ -180,7 +183,14 @@ __global__ void iota_kernel(uint32_t* v, int64_t n) {
 template <class K>
 static int radix_sort_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n, int key_bits,
                         bool identity_values, int64_t* hist, ScanScratch scan, cudaStream_t stream) {
-  const int passes = key_bits <= 0 ? 0 : (key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
+  // digit width: wider digits mean fewer passes but per-tile work (counters,
+  // digit prefix, histogram rows) grows with the radix (TJ_SORT_DIGIT_BITS: A/B)
+  static const int max_bits = [] {
+    const char* e = std::getenv("TJ_SORT_DIGIT_BITS");
+    const int v = e ? std::atoi(e) : kDefaultDigitBits;
+    return v < 4 ? 4 : (v > kMaxDigitBits ? kMaxDigitBits : v);
+  }();
+  const int passes = key_bits <= 0 ? 0 : (key_bits + max_bits - 1) / max_bits;
   if (n <= 1 || passes == 0) {
     if (n > 0 && identity_values) {
       iota_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 4096)), 256, 0, stream>>>(v0, n);

@@ -263,11 +263,15 @@ def row_slice(n: int, rank: int, world: int) -> tuple[int, int]:
     return min(n, rank * per), min(n, (rank + 1) * per)
 
 
-def exchange_counts(ctx, loff, n_local: int, gid, n: int, dev, group=None):
+def exchange_counts(ctx, loff, n_local: int, gid, n: int, dev, group=None, stream=None):
     """Global per-id row counts: every rank scatters its rows' lengths to their
     global ids and the ranks SUM-all-reduce the n counts (each id is owned by one
     rank).  One byte per id while every row is shorter than 256 (a 4-byte MAX
-    all-reduce of the overflow flag decides), else int32."""
+    all-reduce of the overflow flag decides), else int32.
+
+    stream: run the counts' all-reduce there (NCCL), so it overlaps whatever the
+    caller enqueues next on its own stream; the caller waits on `stream` before
+    reading the counts."""
     import torch
     import torch.distributed as dist
 
@@ -285,13 +289,32 @@ def exchange_counts(ctx, loff, n_local: int, gid, n: int, dev, group=None):
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
     if n_local:
         ctx.scatter_counts(loff, n_local, gid, c8, ovf)
-    if int(reduce(ovf, dist.ReduceOp.MAX).item()) == 0:
+    if int(reduce(ovf, dist.ReduceOp.MAX).item()):
+        del c8
+        c8 = torch.zeros(n, dtype=torch.int32, device=dev)
+        if n_local:
+            ctx.scatter_counts(loff, n_local, gid, c8)
+    if stream is None:
         return reduce(c8, dist.ReduceOp.SUM)
-    del c8
-    counts = torch.zeros(n, dtype=torch.int32, device=dev)
-    if n_local:
-        ctx.scatter_counts(loff, n_local, gid, counts)
-    return reduce(counts, dist.ReduceOp.SUM)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(stream):
+        c8 = reduce(c8, dist.ReduceOp.SUM)
+    c8.record_stream(stream)  # used on both streams (gloo returns a copy made on `stream`)
+    c8.record_stream(torch.cuda.current_stream(dev))
+    return c8
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(dev):
+    """One high-priority side stream per device for the collectives that overlap
+    the emit (its NCCL kernels get SM slots before the emit's persistent CTAs)."""
+    import torch
+
+    if dev.index not in _SIDE_STREAMS:
+        _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev, priority=-1)
+    return _SIDE_STREAMS[dev.index]
 
 
 def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> ShardResult:
@@ -332,14 +355,23 @@ def strong_self_join(rows, n: int, d: int, config, group=None, timer=None) -> Sh
         pairs = job.refine(cell_range=(cb, ce))
         mark("refine")
         ctx.set_output_ids(gid)  # rows carry global neighbour ids (gid is monotone)
-        loff, lnbr = job.finalize()
+        # local row offsets first: the global counts they give are all-reduced on a
+        # side stream while this rank's rows are emitted
+        loff = torch.empty(n_local + 1, dtype=torch.int64, device=dev)
+        lnbr = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
+        job.offsets_d, job.neighbors_d = loff, lnbr
+        ctx.finalize_offsets(loff)
+        side = _side_stream(dev)
+        counts = exchange_counts(ctx, loff, n_local, gid, n, dev, group, stream=side)
+        ctx.finalize_rows(loff, lnbr)
+        torch.cuda.current_stream(dev).wait_stream(side)
     else:
         cb = ce = 0
         loff = torch.zeros(1, dtype=torch.int64, device=dev)
         lnbr = torch.empty(1, dtype=torch.int32, device=dev)
         mark("index")
         mark("refine")
-    counts = exchange_counts(ctx, loff, n_local, gid, n, dev, group)
+        counts = exchange_counts(ctx, loff, n_local, gid, n, dev, group)
     goff = torch.empty(n + 1, dtype=torch.int64, device=dev)
     ctx.counts_to_offsets(counts, n, goff)
     mark("offsets")

@@ -22,3 +22,11 @@ for l in open(out+"/sweep.jsonl"):
 d=json.loads(open(out+"/bench.json").read().strip().splitlines()[-1])
 print("bench", round(d["ms_per_step"],4), d.get("phases_ms"), "e2e", d["e2e"].get("seconds"))
 P
+timeout 900 python tools/strong_projection.py c5 2 4 8 > "$out/strong_projection.jsonl" 2> "$out/strong_projection.err"; echo "projection rc=$?" >> "$out/status.txt"
+python - "$out" <<'P'
+import json,sys
+for l in open(sys.argv[1]+"/strong_projection.jsonl"):
+    x=json.loads(l)
+    if "G" in x: print(x["G"], round(x["T_G_ms"],2), "eff", round(x["efficiency"],3), "serial", round(x["efficiency_serial_collectives"],3), {k:round(v,3) for k,v in x["slowest_rank"].items() if k.endswith("_ms")})
+    else: print("T1", x["T1_ms"])
+P

@@ -39,9 +39,28 @@ n_local = ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_
 local = torch.empty((n_local, coords.shape[1]), dtype=torch.float64, device=dev)
 gid = torch.empty(n_local, dtype=torch.int32, device=dev)
 ctx.shard_select(coords, n, d, pdims, eps, plan.origin, plan.span, lo_b, hi_b, out=local, gid=gid)
+# the rank's routing of its own row slice (distributed.exchange_points, this side)
+per = -(-n // G)
+sl = coords[r * per: min(n, (r + 1) * per)]
+rt = []
+for i in range(6):
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    cnts = ctx.shard_route(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, plan.ranges)
+    e[1].record()
+    send = torch.empty((max(sum(cnts), 1), coords.shape[1]), dtype=torch.float64, device=dev)
+    sgid = torch.empty(max(sum(cnts), 1), dtype=torch.int32, device=dev)
+    ctx.shard_route(sl, sl.shape[0], d, pdims, eps, plan.origin, plan.span, plan.ranges,
+                    counts=cnts, out=send, gid=sgid, gid_base=r * per)
+    e[2].record()
+    torch.cuda.synchronize()
+    rt.append([e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])])
+    del send, sgid
+rm = np.median(np.array(rt[1:]), axis=0)
+print(f"G={G} rank={r}: route count {rm[0]:.3f} ms, route write {rm[1]:.3f} ms", flush=True)
 cfg = JoinConfig(epsilon=eps)
 wrap = Dataset._wrap(np.empty((n_local, coords.shape[1])), d)
-del coords
+del coords, sl
 torch.cuda.synchronize()
 rows = []
 for i in range(reps):
