@@ -8,7 +8,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-src = Path(sys.argv[1])
+src = Path(sys.argv[1]).resolve()
 rows = [r for v in json.load(open(src)).values() for r in v]
 out = {}
 for key in ("refine_lowd_kernel", "count_rows_kernel", "emit_rows_kernel"):
