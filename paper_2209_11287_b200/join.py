@@ -442,19 +442,33 @@ class DeviceJoin:
         torch.cuda.current_stream(self.device).synchronize()
         return off.numpy(), nbr.numpy()
 
-    def finalize_fetch(self, chunks: int = 8):
+    # id ranges of the result pipeline, one D2H copy each (measured at c2,
+    # profiles/r2aj/e2e_pipeline.txt: 16 ranges 10.46 ms for rows + copies, 8
+    # ranges 10.64; grouping ranges into growing copies leaves a long last copy
+    # exposed: 12.0)
+    PIPELINE_CHUNKS = 16
+    PIPELINE_COPIES = None
+
+    def finalize_fetch(self, chunks: int | None = None, copies=None):
         """finalize() + fetch() as a pipeline into pinned host memory; returns numpy
         (offsets, neighbors).
 
         The offsets go first (their D2H on the copy stream overlaps the first rows).
         The rows are then built in `chunks` ranges of original ids
         (tj_finalize_rows_chunk): each range is one contiguous part of the CSR, final
-        when its kernels end, and its D2H on the copy stream overlaps the next range's
-        emit -- the double-buffered result pipeline of the north star, with the PCIe
-        copy engine running while the SMs emit."""
+        when its kernels end.  The ranges are copied in groups (`copies`: ranges per
+        D2H, summing to `chunks`) on a copy stream while the next ranges are emitted
+        -- the double-buffered result pipeline of the north star, with the PCIe copy
+        engine running while the SMs emit."""
         torch = self.torch
         n = self.work.n
         dev = f"cuda:{self.device}"
+        if chunks is None:
+            chunks, copies = self.PIPELINE_CHUNKS, self.PIPELINE_COPIES
+        if copies is None:
+            copies = (1,) * chunks
+        if sum(copies) != chunks:
+            raise ValueError("copies must sum to chunks")
         main = torch.cuda.current_stream(self.device)
         self.offsets_d = torch.empty(n + 1, dtype=torch.int64, device=dev)
         self.neighbors_d = torch.empty(max(self.total, 1), dtype=torch.int32, device=dev)
@@ -470,14 +484,17 @@ class DeviceJoin:
             off_ready = torch.cuda.Event()
             off_ready.record(cs)
         bounds = [(k * n + chunks - 1) // chunks for k in range(chunks + 1)]  # tj_finalize_rows_chunk
-        for k in range(chunks):
-            a, b = bounds[k], bounds[k + 1]
-            self.ctx.finalize_rows_chunk(self.offsets_d, self.neighbors_d, k, chunks)
+        k = 0
+        for g, m in enumerate(copies):
+            k0 = k
+            for _ in range(m):
+                self.ctx.finalize_rows_chunk(self.offsets_d, self.neighbors_d, k, chunks)
+                k += 1
             done = torch.cuda.Event()
             done.record(main)
-            if k == 0:
+            if g == 0:
                 off_ready.synchronize()  # host needs the offsets to size the copies
-            lo, hi = int(off[a]), int(off[b])
+            lo, hi = int(off[bounds[k0]]), int(off[bounds[k]])
             if hi > lo:
                 cs.wait_event(done)
                 with torch.cuda.stream(cs):

@@ -29,7 +29,8 @@ def sync():
     return time.perf_counter()
 
 
-for chunks in (1, 2, 4, 8, 16):
+for chunks, copies in ((1, None), (8, None), (16, None), (24, None), (32, None),
+                       (32, (1, 2, 4, 8, 17))):
     rows = []
     for r in range(reps):
         t0 = sync()
@@ -40,11 +41,11 @@ for chunks in (1, 2, 4, 8, 16):
         t2 = sync()
         job.refine()
         t3 = sync()
-        off, nbr = job.finalize_fetch(chunks=chunks)
+        off, nbr = job.finalize_fetch(chunks=chunks, copies=copies)
         t4 = sync()
         rows.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3, t4 - t0))
     m = np.median(np.array(rows), axis=0) * 1e3
-    print(f"{name} chunks={chunks:2d}: upload {m[0]:.2f} build {m[1]:.2f} refine {m[2]:.2f} "
+    print(f"{name} chunks={chunks:2d} copies={copies}: upload {m[0]:.2f} build {m[1]:.2f} refine {m[2]:.2f} "
           f"finalize+fetch {m[3]:.2f} | total {m[4]:.2f} ms", flush=True)
 ts = []
 for r in range(reps):
