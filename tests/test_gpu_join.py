@@ -447,6 +447,23 @@ def test_split_finalize_matches_one_call(d, kernel):
     assert csr_equal(off_a, nbr_a, off, nb)
 
 
+@pytest.mark.parametrize("chunks,copies", [(1, None), (5, None), (16, None), (32, (1, 2, 4, 8, 17)),
+                                           (7, (3, 4))])
+def test_result_pipeline_schedules(chunks, copies):
+    """Any id-range split and D2H copy grouping of the result pipeline gives the same CSR."""
+    from paper_2209_11287_b200.join import DeviceJoin
+
+    ds = generate(GenSpec("uniform", 20000, 3, seed=8))
+    eps = 0.06
+    job = DeviceJoin(ds, JoinConfig(epsilon=eps), device=0)
+    job.build()
+    job.refine()
+    off_a, nbr_a = job.finalize_fetch(chunks=chunks, copies=copies)
+    job.finalize()
+    off_b, nbr_b = job.fetch()
+    assert np.array_equal(off_a, off_b) and np.array_equal(nbr_a, nbr_b)
+
+
 @pytest.mark.parametrize("kernel", ALL_KERNELS)
 @pytest.mark.parametrize("d", [2, 3, 4, 8])
 def test_lattice_boundary_pairs(kernel, d):
