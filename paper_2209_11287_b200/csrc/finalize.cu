@@ -97,7 +97,7 @@ __device__ __forceinline__ void warp_sort_row(uint32_t* row, int len) {
   }
 }
 
-constexpr int kWarpSortMax = 256;
+constexpr int kWarpSortMax = 1024;
 constexpr int kBlockSortMax = 8192;
 
 // ---------------------------------------------------------------- row batches
@@ -191,7 +191,9 @@ __device__ __noinline__ void pool_sort(uint32_t* pool, int len) {
 __device__ __noinline__ void sort_long_row(uint32_t* row, int len, uint32_t id, uint32_t* big_rows,
                                            unsigned long long* n_big) {
   if (len <= 128) warp_sort_row<4>(row, len);
-  else if (len <= kWarpSortMax) warp_sort_row<8>(row, len);
+  else if (len <= 256) warp_sort_row<8>(row, len);
+  else if (len <= 512) warp_sort_row<16>(row, len);
+  else if (len <= kWarpSortMax) warp_sort_row<32>(row, len);
   else if (lane_id() == 0) big_rows[atomicAdd(n_big, 1ull)] = id;
 }
 
@@ -757,7 +759,26 @@ __global__ void __launch_bounds__(256)
     __syncwarp();
     const int64_t rb = cell_runs[c];
     const int nr = int(cell_runs[c + 1] - rb);
-    for (int e = lane; e < base; e += 32) row[e] = nid[run_position(runs, run_off, rb, nr, row[e])];
+    if (nr <= 32) {
+      // the cell's runs in the lanes (lane r: run r); each offset finds its run
+      // by a 5-step search over the lanes (no dependent global loads)
+      const uint32_t ro = lane < nr ? run_off[rb + lane] : 0xffffffffu;
+      const uint32_t rp = lane < nr ? runs[rb + lane].x : 0u;
+      for (int e0 = 0; e0 < base; e0 += 32) {
+        const int e = e0 + lane;
+        const uint32_t t = e < base ? row[e] : 0u;
+        int r = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t o = __shfl_sync(0xffffffffu, ro, r + step);
+          if (o <= t) r += step;
+        }
+        const uint32_t pos = __shfl_sync(0xffffffffu, rp, r) + (t - __shfl_sync(0xffffffffu, ro, r));
+        if (e < base) row[e] = nid[pos];
+      }
+    } else {
+      for (int e = lane; e < base; e += 32) row[e] = nid[run_position(runs, run_off, rb, nr, row[e])];
+    }
     // symmetric join: the pairs with earlier neighbour cells (rare long rows: one lane)
     if (sym.fwd && lane == 0) {
       int at = base;
