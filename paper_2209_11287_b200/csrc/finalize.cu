@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
                      const uint32_t* __restrict__ qcount, const uint32_t* __restrict__ perm,
                      const uint32_t* __restrict__ nid,
                      const int64_t* __restrict__ offsets, int64_t n, uint32_t* __restrict__ nbr,
-                     uint32_t* __restrict__ long_rows, unsigned long long* n_long, RowList rl,
+                     uint2* __restrict__ long_rows, unsigned long long* n_long, RowList rl,
                      SymTables sym) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, MINB)
       c_last = __shfl_sync(0xffffffffu, c, 31);
     }
     const bool pooled = len > 0 && len <= kPoolSlots;
-    if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = uint32_t(p);
+    if (len > kPoolSlots) long_rows[atomicAdd(n_long, 1ull)] = make_uint2(uint32_t(p), uint32_t(c));
     MaskRow mr{};
     if (pooled) {
       mr = mask_row(masks, cell_mbase, cell_cand, c, p - cell_start[c], sym.fwd);
@@ -717,20 +717,15 @@ __global__ void __launch_bounds__(256)
                      int64_t n_cells, const uint32_t* __restrict__ perm,
                      const uint32_t* __restrict__ nid,
                      const int64_t* __restrict__ offsets, uint32_t* __restrict__ nbr,
-                     const uint32_t* __restrict__ long_rows, const unsigned long long* n_long,
+                     const uint2* __restrict__ long_rows, const unsigned long long* n_long,
                      uint32_t* __restrict__ big_rows, unsigned long long* n_big, SymTables sym) {
   const int lane = lane_id();
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const int64_t nl = int64_t(*n_long);
   for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32; i < nl; i += warps) {
-    const uint32_t p = long_rows[i];
-    int64_t lo = 0, hi = n_cells;  // cell containing p
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (cell_start[mid] <= p) lo = mid;
-      else hi = mid;
-    }
-    const int64_t c = lo;
+    const uint2 pc = long_rows[i];  // (position, its cell), listed by the emit kernel
+    const uint32_t p = pc.x;
+    const int64_t c = pc.y;
     const uint32_t id = perm[p];
     const int64_t dst = offsets[id];
     const int len = int(offsets[id + 1] - dst);
@@ -1152,7 +1147,7 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
   unsigned long long* nbig = reinterpret_cast<unsigned long long*>(ctx->minmax.as<long long>());
   TJ_CUDA(cudaMemsetAsync(nbig, 0, 3 * sizeof(unsigned long long), s));
   ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
-  uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
+  uint2* long_rows = reinterpret_cast<uint2*>(ctx->pos_off.as<int64_t>());
   if (le > lb) {
     auto kern = emit_rows_kernel<8, true>;
     const size_t smem = sizeof(EmitSmem) * kEmitWarps;
@@ -1170,7 +1165,7 @@ void finalize_rows_range(tj_ctx* ctx, const int64_t* offsets, uint32_t* nbr, int
         neighbour_ids(ctx, s), offsets, n, nbr, long_rows, nbig + 2, rl, sym_tables(ctx));
     TJ_CHECK_LAUNCH();
   }
-  long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
+  long_rows_kernel<<<kNumSMs * 3, 256, 0, s>>>(
       ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
       ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
       ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), ctx->g.n_cells,
@@ -1210,7 +1205,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
     const int64_t nc = ctx->g.n_cells;
     const int64_t n_win = ceil_div(n, 32);
     ctx->pos_off.ensure(sizeof(int64_t) * (n + 1), s);
-    uint32_t* long_rows = reinterpret_cast<uint32_t*>(ctx->pos_off.as<int64_t>());
+    uint2* long_rows = reinterpret_cast<uint2*>(ctx->pos_off.as<int64_t>());
     {
       // 4 CTAs/SM (<= 128 registers): measured on par with the unbounded build
       // (158 registers, 3 CTAs) and well ahead of 5 CTAs (spills)
@@ -1234,7 +1229,7 @@ void finalize_csr(tj_ctx* ctx, int64_t* offsets, uint32_t* nbr, int64_t n_pairs,
       TJ_CUDA(cudaEventRecord(ctx->ev3, s));
       ctx->have_emit_timing = true;
     }
-    long_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(
+    long_rows_kernel<<<kNumSMs * 3, 256, 0, s>>>(
         ctx->masks.as<unsigned long long>(), ctx->cell_mbase.as<int64_t>(),
         ctx->cell_start.as<int64_t>(), ctx->cell_runs.as<int64_t>(), ctx->runs.as<uint2>(),
         ctx->run_off.as<uint32_t>(), ctx->cell_cand.as<int64_t>(), nc, ctx->perm.as<uint32_t>(),
