@@ -205,41 +205,66 @@ __global__ void route_tile_count_kernel(const unsigned long long* __restrict__ d
   }
 }
 
+// One pass over the tile's rows: every 32-row round loads its destination
+// masks and rows once, then places the rows of each destination present in the
+// round (ballot rank = stable order) -- no per-destination re-walk of the tile.
+// The per-destination cursors live in shared memory (G <= 64).
 template <bool VEC>
-__global__ void route_tile_write_kernel(const unsigned long long* __restrict__ dest, int64_t n,
-                                        int G, int64_t n_tiles, const int64_t* __restrict__ tile_off,
-                                        const double* __restrict__ x, int64_t ld, int d,
-                                        double* __restrict__ out, int64_t ld_out,
-                                        uint32_t* __restrict__ gid, int64_t gid_base) {
+__global__ void __launch_bounds__(256)
+    route_tile_write_kernel(const unsigned long long* __restrict__ dest, int64_t n, int G,
+                            int64_t n_tiles, const int64_t* __restrict__ tile_off,
+                            const double* __restrict__ x, int64_t ld, int d,
+                            double* __restrict__ out, int64_t ld_out, uint32_t* __restrict__ gid,
+                            int64_t gid_base) {
+  __shared__ int64_t s_at[8][64];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  int64_t* at = s_at[warp];
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   const unsigned lt = lanemask_lt();
   for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < n_tiles; t += warps) {
     const int64_t i0 = t * kRouteRows, i1 = min(n, (t + 1) * kRouteRows);
-    unsigned long long any = 0;  // destinations present in the tile
-    for (int64_t i = i0 + lane_id(); i < i1; i += 32) any |= dest[i];
+    __syncwarp();
+    for (int r = lane; r < G; r += 32) at[r] = tile_off[int64_t(r) * n_tiles + t];
+    __syncwarp();
+    for (int64_t base = i0; base < i1; base += 32) {
+      const int64_t i = base + lane;
+      const unsigned long long m = i < i1 ? dest[i] : 0ull;
+      double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+      if (VEC && m) {
+        const double2* src = reinterpret_cast<const double2*>(x + i * ld);
+        v0 = __ldg(src);
+        if (ld_out > 2) v1 = __ldg(src + 1);
+      }
+      unsigned long long present = m;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
-    while (any) {
-      const int r = __ffsll(any) - 1;
-      any &= any - 1ull;
-      int64_t at = tile_off[int64_t(r) * n_tiles + t];
-      for (int64_t base = i0; base < i1; base += 32) {
-        const int64_t i = base + lane_id();
-        const bool hit = i < i1 && ((dest[i] >> r) & 1ull);
+      for (int o = 16; o > 0; o >>= 1) present |= __shfl_xor_sync(0xffffffffu, present, o);
+      while (present) {
+        const int r = __ffsll(present) - 1;
+        present &= present - 1ull;
+        const bool hit = (m >> r) & 1ull;
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        const int64_t a = at[r];
         if (hit) {
-          const int64_t o = at + __popc(bal & lt);
-          const double* src = x + i * ld;
+          const int64_t o = a + __popc(bal & lt);
           double* dst = out + o * ld_out;
-          if (VEC) {  // rows of d == ld == ld_out doubles, 16-byte aligned
-            for (int j = 0; j < ld_out; j += 2)
-              *reinterpret_cast<double2*>(dst + j) = __ldg(reinterpret_cast<const double2*>(src + j));
+          if (VEC) {
+            if (ld_out == 4) {
+              reinterpret_cast<double2*>(dst)[0] = v0;
+              reinterpret_cast<double2*>(dst)[1] = v1;
+            } else {
+              const double* src = x + i * ld;
+              for (int j = 0; j < ld_out; j += 2)
+                *reinterpret_cast<double2*>(dst + j) = __ldg(reinterpret_cast<const double2*>(src + j));
+            }
           } else {
+            const double* src = x + i * ld;
             for (int j = 0; j < ld_out; ++j) dst[j] = j < d ? src[j] : 0.0;
           }
           gid[o] = uint32_t(gid_base + i);
         }
-        at += __popc(bal);
+        __syncwarp();
+        if (lane == 0) at[r] = a + __popc(bal);
+        __syncwarp();
       }
     }
   }

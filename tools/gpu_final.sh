@@ -17,7 +17,7 @@ timeout 2400 python tools/sweep.py c1 c2 c4d2 c4d8 c3 c5 expo3d2m --reps 2 --ker
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $out/launches_c2.csv python bench.py --steps 1 --warmup 3 --skip-cpu > $out/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $out/status.txt
 python tools/launch_summary.py $out/launches_c2.csv > $out/launches_c2_summary.txt 2>> $out/status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:refine_lowd|emit_rows|count_rows" -c 3 \
+timeout 900 ncu -f --set full --clock-control none --import-source on -k "regex:refine_lowd|emit_rows|count_rows" -c 3 \
   -o /tmp/full_c2 python bench.py --steps 1 --warmup 3 --skip-cpu > $out/ncu_full.log 2>&1; echo "ncu full rc=$?" >> $out/status.txt
 python tools/ncu_summary.py /tmp/full_c2.ncu-rep > $out/ncu_full_c2.json 2>> $out/status.txt
 timeout 600 python tools/shard_index_probe.py 8 7 10 > $out/shard_index.txt 2>&1
