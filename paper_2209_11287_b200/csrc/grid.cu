@@ -511,6 +511,42 @@ __global__ void cand_count_kernel(RowParams rp, const uint64_t* __restrict__ cel
     }
     return;
   }
+  if (use_gallop(rp) && rp.n_rows <= 16) {
+    // k_idx <= 3: each half-warp walks every other cell of the warp's range
+    // (lane = row), so 2 cells per step instead of one with half the lanes idle
+    const int64_t per = (n_cells + warps - 1) / warps;
+    const int64_t cb = w0 * per, ce = min(n_cells, cb + per);
+    const int h = int(lane_id()) >> 4, r = int(lane_id()) & 15;
+    int64_t pa = 0, pz = 0;
+    for (int64_t c0 = cb; c0 < ce; c0 += 2) {
+      const int64_t c = c0 + h;
+      const bool vc = c < ce;
+      int64_t runs = 0, cands = 0;
+      if (vc && r < rp.n_rows) {
+        uint64_t lo, hi;
+        row_key_range(rp, cell_key[c], r, lo, hi);
+        const int64_t a = gallop_lb(cell_key, n_cells, lo, pa);
+        const int64_t z = gallop_ub(cell_key, n_cells, hi, max(pz, a));
+        pa = a;
+        pz = z;
+        const int64_t b = cell_start[a], e = cell_start[z];
+        if (e > b) {
+          runs = 1;
+          cands = e - b;
+        }
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {  // sums inside each half
+        runs += __shfl_xor_sync(0xffffffffu, runs, o);
+        cands += __shfl_xor_sync(0xffffffffu, cands, o);
+      }
+      if (r == 0 && vc) {
+        run_count[c] = runs;
+        cand_count[c] = cands;
+      }
+    }
+    return;
+  }
   if (use_gallop(rp)) {  // contiguous cells per warp, galloping row searches
     const int64_t per = (n_cells + warps - 1) / warps;
     const int64_t cb = w0 * per, ce = min(n_cells, cb + per);
@@ -600,6 +636,42 @@ __global__ void cand_fill_kernel(RowParams rp, const uint64_t* __restrict__ cell
           runs[out[u] + __popc(m & lt)] = make_uint2(uint32_t(b[u]), uint32_t(e[u]));
           run_off[out[u] + __popc(m & lt)] = uint32_t(inc - len);
         }
+      }
+    }
+    return;
+  }
+  if (use_gallop(rp) && rp.n_rows <= 16) {  // two cells per step, one per half-warp
+    const int64_t per = (n_cells + warps - 1) / warps;
+    const int64_t cb = w0 * per, ce = min(n_cells, cb + per);
+    const int h = int(lane_id()) >> 4, r = int(lane_id()) & 15;
+    const unsigned lt16 = (1u << r) - 1u;
+    int64_t pa = 0, pz = 0;
+    for (int64_t c0 = cb; c0 < ce; c0 += 2) {
+      const int64_t c = c0 + h;
+      const bool vc = c < ce;
+      int64_t b = 0, e = 0, out = 0;
+      if (vc && r < rp.n_rows) {
+        uint64_t lo, hi;
+        row_key_range(rp, cell_key[c], r, lo, hi);
+        const int64_t a = gallop_lb(cell_key, n_cells, lo, pa);
+        const int64_t z = gallop_ub(cell_key, n_cells, hi, max(pz, a));
+        pa = a;
+        pz = z;
+        b = cell_start[a];
+        e = cell_start[z];
+        out = cell_runs[c];
+      }
+      const unsigned mh = (__ballot_sync(0xffffffffu, e > b) >> (16 * h)) & 0xffffu;
+      const int64_t len = e - b;
+      int64_t inc = len;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {  // inclusive scan inside each half
+        const int64_t t = __shfl_up_sync(0xffffffffu, inc, o, 16);
+        if (r >= o) inc += t;
+      }
+      if (e > b) {
+        runs[out + __popc(mh & lt16)] = make_uint2(uint32_t(b), uint32_t(e));
+        run_off[out + __popc(mh & lt16)] = uint32_t(inc - len);
       }
     }
     return;
